@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark: B-spline VGH orbital-evals/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config 4] [--chunk 65536] [--mode fast] [--tile 0]
+
+Workload (default, BASELINE config 4 -- the VGH config with N >= 2048 the
+north-star roofline target names): 64^3 periodic grid (67^3 wrap-padded),
+N = 4096 fp32 orbitals, FillSpec.random(0) table (generated on the device,
+bit-identical to the reference's numpy fill), 4096 walkers x 256 moves =
+1,048,576 VGH positions per GPU per step (Philox walker streams, seed 1).
+A step evaluates all of them, in launches of `--chunk` positions into a
+reusable output buffer (every output is written to HBM; the reference also
+overwrites its output buffer per position, kernels.py:353-354).
+
+Multi-GPU (torchrun, one rank per GPU): walker-sharded, table replicated,
+each rank evaluates its own 4096-walker population (weak scaling), no
+collective on the data path; time = max over ranks.
+
+Printed JSON (rank 0): value = orbital-evals/s over all ranks; roofline of
+the eval kernel (algorithmic bytes 64*Npad*4 + 10*Npad*4 per position over
+the measured HBM copy bandwidth); e2e through the drop-in API eval_batch with
+host buffers; cpu_baseline = the C restatement of the reference fp32 kernels
+(oracle/, kind "port") on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "B-spline VGH orbital-evals/s"
+UNIT = "orbital-evals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--kind", default=None, help="override the config kernel (v/vgl/vgh)")
+    ap.add_argument("--chunk", type=int, default=1 << 16)
+    ap.add_argument("--mode", default="fast", choices=("fast", "strict"))
+    ap.add_argument("--tile", type=int, default=0, help="AoSoA tile size (0 = untiled)")
+    ap.add_argument("--walkers", type=int, default=0, help="override walkers per GPU")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def workload(args, rank):
+    from paper_1611_02665_b200.workloads import CONFIGS, bytes_per_position, walker_positions
+
+    cfg = CONFIGS[args.config]
+    if cfg.dtype != "f32" or cfg.index == 5:
+        raise SystemExit("bench.py times the fp32 walker-sharded configs (1-4)")
+    kind = args.kind or ("vgh" if cfg.kernel == "vgh" else cfg.kernel)
+    walkers = args.walkers or cfg.walkers
+    first = rank * walkers
+    pos = walker_positions(1, range(first, first + walkers), 0, kind, cfg.moves, cfg.grid)
+    return cfg, kind, pos, bytes_per_position(kind, cfg.n_splines)
+
+
+def cpu_baseline(table_soa, grid, kind, pos, n_splines, budget_s, threads=0):
+    """Reference fp32 kernels restated in C (oracle/), all host threads, with
+    the reference's batch semantics (each thread overwrites its own output
+    buffer, kernels.py:353-354).  Calibrated to ~budget_s of CPU work."""
+    import oracle
+
+    threads = threads or oracle.host_threads()
+    spac = grid.spacings
+    oracle.eval_f32(kind, table_soa, spac, pos[: 4 * threads], overwrite=True, nthreads=threads)  # warm
+    n = 8 * threads
+    while True:
+        t0 = time.perf_counter()
+        oracle.eval_f32(kind, table_soa, spac, pos[:n], overwrite=True, nthreads=threads)
+        dt = time.perf_counter() - t0
+        if dt > 0.5 or n >= pos.shape[0]:
+            break
+        n = min(pos.shape[0], n * 4)
+    n_final = int(min(pos.shape[0], max(n, n * budget_s / max(dt, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.eval_f32(kind, table_soa, spac, pos[:n_final], overwrite=True, nthreads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": n_final * n_splines / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{n_final} of the workload's positions x N={n_splines} {kind.upper()}, "
+                      f"{dt:.1f} s, C restatement of kernels.py fp32 kernels (oracle/spline_oracle.c, "
+                      f"-O3 AVX2/AVX-512 clones, OpenMP)"}
+
+
+def host_reference_table(cfg, seed=0):
+    """Reference-layout fp32 table with U[-1,1) values for the CPU arms
+    (values do not change the reference kernels' speed)."""
+    from paper_1611_02665_b200.coeffs import padded_count
+
+    nx, ny, nz = cfg.grid.counts
+    npad = padded_count(cfg.n_splines)
+    rng = np.random.default_rng(seed)
+    data = rng.random((nx, ny, nz, npad), dtype=np.float32)
+    data *= np.float32(2.0)
+    data -= np.float32(1.0)
+    data[..., cfg.n_splines:] = 0.0
+    return data
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1611_02665_b200.workloads import CONFIGS, walker_positions
+
+    import oracle
+
+    cfg = CONFIGS[args.config]
+    kind = args.kind or cfg.kernel
+    threads = oracle.host_threads()
+    table = host_reference_table(cfg)
+    # each step: a bounded sample of the workload, sized to ~ budget seconds
+    per_step_budget = max(1.0, min(8.0, 150.0 / max(1, args.steps + args.warmup)))
+    pos = walker_positions(1, range(0, 256), 0, kind, cfg.moves, cfg.grid)
+    probe = cpu_baseline(table, cfg.grid, kind, pos, cfg.n_splines, 1.0, threads)
+    n = int(min(pos.shape[0], max(threads, probe["value"] / cfg.n_splines * per_step_budget)))
+    sample = pos[:n]
+    for _ in range(args.warmup):
+        oracle.eval_f32(kind, table, cfg.grid.spacings, sample, overwrite=True, nthreads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.eval_f32(kind, table, cfg.grid.spacings, sample, overwrite=True, nthreads=threads)
+    dt = time.perf_counter() - t0
+    value = n * cfg.n_splines * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC if kind == "vgh" else f"B-spline {kind.upper()} orbital-evals/s",
+        "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (U[-1,1) table, Philox walker positions)",
+        "config": {"workload": f"cfg{cfg.index}: {cfg.description}", "positions_per_step": n,
+                   "grid": list(cfg.grid.counts), "n_splines": cfg.n_splines, "kernel": kind},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{n} positions per step x {args.steps} steps; reference fp32 kernels "
+                                   "restated in C (oracle/spline_oracle.c), reference has no C build "
+                                   "(numba JIT, cannot travel)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args):
+    import torch
+
+    world, rank, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py --impl b200 needs a CUDA device")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1611_02665_b200 import DeviceTable, KernelKind, WalkerOutputsSoA, eval_batch, evaluate
+
+    cfg, kind, pos_np, bpp = workload(args, rank)
+    P = pos_np.shape[0]
+    N = cfg.n_splines
+    S = KernelKind(kind).output_streams_soa
+    table = DeviceTable.random(cfg.grid, N, seed=0, tile_size=args.tile or None, device=dev)
+    pos = torch.from_numpy(pos_np).to(dev)
+    chunk = min(args.chunk, P)
+    out = torch.empty((chunk, S, table.lanes), dtype=torch.float32, device=dev)
+    bounds = [(lo, min(P, lo + chunk)) for lo in range(0, P, chunk)]
+    stream = torch.cuda.current_stream(dev)
+
+    def step(events=None):
+        for b, (lo, hi) in enumerate(bounds):
+            if events is not None:
+                events[b][0].record(stream)
+            evaluate(table, kind, pos[lo:hi], out, mode=args.mode, check=False)
+            if events is not None:
+                events[b][1].record(stream)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # correctness guard on the benchmarked configuration (one launch)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    evaluate(table, kind, pos[:chunk], out, mode=args.mode, status=status, check=False)
+    assert int(status.item()) == 0
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    launch_events = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                      for _ in bounds] for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        t_start.record(stream)
+        for k in range(args.steps):
+            step(launch_events[k])
+        t_end.record(stream)
+        barrier()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    launch_ms = [s.elapsed_time(e) for ev in launch_events for (s, e) in ev]
+    full = [ms for (lo, hi), ms in zip(bounds * args.steps, launch_ms) if hi - lo == chunk]
+    avg_launch_ms = sum(full) / len(full)
+
+    # max over ranks
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    total_units = P * N * args.steps * world
+    value = total_units / (elapsed_ms / 1e3)
+
+    peak, peak_src = measured_peak()
+    achieved = bpp * chunk / (avg_launch_ms / 1e-3) / 1e9  # GB/s per launch
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(args, cfg, kind, chunk),
+                "peak_source": peak_src, "kernel": f"spo::eval_kernel<{kind.upper()},float,{args.mode}>",
+                "algorithmic_bytes_per_position": bpp, "positions_per_launch": chunk,
+                "avg_launch_ms": avg_launch_ms}
+
+    result = {
+        "metric": METRIC if kind == "vgh" else f"B-spline {kind.upper()} orbital-evals/s",
+        "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: FillSpec.random(0) table generated on device (bit-identical to the "
+                "reference numpy fill), reference Philox walker position streams (seed 1)",
+        "config": {"workload": f"cfg{cfg.index}: {cfg.description}", "grid": list(cfg.grid.counts),
+                   "n_splines": N, "kernel": kind, "positions_per_gpu": P, "walkers_per_gpu": P // cfg.moves,
+                   "chunk": chunk, "mode": args.mode, "tile_size": table.tile_size,
+                   "table_gb": table.nbytes / 1e9,
+                   "l2": f"inputs larger than L2 (table {table.nbytes / 1e9:.2f} GB >> 126 MB); no flush",
+                   "parallelism": f"walker-sharded x{world}, table replicated"},
+        "roofline": roofline,
+        "gpu_launches": len(bounds) * args.steps,
+        "clocks": clocks.summary(),
+    }
+
+    if rank == 0 and not args.no_e2e:
+        result["e2e"] = e2e_dropin(table, kind, pos_np, N, S, eval_batch, WalkerOutputsSoA, args, dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    if rank == 0 and world == 1 and not args.no_cpu:
+        soa = table.reference_soa()
+        result["cpu_baseline"] = cpu_baseline(soa, cfg.grid, kind, pos_np, N, args.cpu_seconds)
+        del soa
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_dropin(table, kind, pos_np, N, S, eval_batch, WalkerOutputsSoA, args, dev):
+    """Same metric through the reference-facing drop-in call eval_batch with
+    HOST buffers: host positions -> device each step, all positions evaluated,
+    the last position's streams copied back into the host WalkerOutputsSoA
+    (the reference API's output, kernels.py:353-354).  Timed by wall clock
+    around fully synchronous calls (the call returns host data)."""
+    import torch
+
+    out = WalkerOutputsSoA(N)
+    steps = max(2, min(args.steps, 3))
+    eval_batch(table, kind, pos_np, out, mode=args.mode)  # warm
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        eval_batch(table, kind, pos_np, out, mode=args.mode)
+    dt = time.perf_counter() - t0
+    P = pos_np.shape[0]
+    return {"value": P * N * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(pos_np.nbytes),
+            "d2h_bytes_per_step": int(S * table.lanes * 4),
+            "api": "paper_1611_02665_b200.eval_batch(table, kind, host positions, host WalkerOutputsSoA)"}
+
+
+def ncu_traffic(args, cfg, kind, chunk):
+    """dram read+write bytes per launch from the committed ncu capture, when
+    it was taken on this exact configuration (profiles/ncu_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            rec = json.load(f)
+        key = f"cfg{cfg.index}-{kind}-{args.mode}-tile{args.tile}"
+        r = rec.get(key)
+        if r and r.get("positions_per_launch") == chunk:
+            return r["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    return None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,75 @@
+// spo_common.cuh -- shared host/device helpers for libspo_b200.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/spo_b200.h"
+
+namespace spo {
+
+// Thread-local last-error text (spo_last_error).
+inline std::string &last_error_slot() {
+    static thread_local std::string s;
+    return s;
+}
+
+inline int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    last_error_slot() = buf;
+    return code;
+}
+
+inline int ok() {
+    last_error_slot().clear();
+    return SPO_OK;
+}
+
+inline int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SPO_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return ok();
+}
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+inline int dtype_size(int dtype) { return dtype == SPO_F64 ? 8 : 4; }
+
+// Device table geometry shared by the eval, pack and fill kernels.
+struct TableGeom {
+    int nx, ny, nz;        // reference grid counts
+    int nxp, nyp, nzp;     // wrap-padded counts (n + 3)
+    int nb;                // row length (lanes) per tile
+    int n_tiles;
+    long long tile_stride; // elements per tile
+};
+
+inline int make_geom(const int32_t *n3, int32_t nb, int32_t n_tiles, int dtype, TableGeom *g) {
+    if (!n3) return fail(SPO_ERR_CONTRACT, "grid counts pointer is NULL");
+    for (int a = 0; a < 3; ++a)
+        if (n3[a] < 4) return fail(SPO_ERR_CONFIG, "grid count %d on axis %d must be >= 4", n3[a], a);
+    const int quantum = dtype == SPO_F64 ? 16 : 32;  // 128-byte rows
+    if (nb <= 0 || nb % quantum)
+        return fail(SPO_ERR_CONTRACT, "row length nb=%d must be a positive multiple of %d", nb,
+                    quantum);
+    if (n_tiles <= 0) return fail(SPO_ERR_CONFIG, "n_tiles=%d must be >= 1", n_tiles);
+    g->nx = n3[0];
+    g->ny = n3[1];
+    g->nz = n3[2];
+    g->nxp = n3[0] + 3;
+    g->nyp = n3[1] + 3;
+    g->nzp = n3[2] + 3;
+    g->nb = nb;
+    g->n_tiles = n_tiles;
+    g->tile_stride = (long long)g->nxp * g->nyp * g->nzp * nb;
+    return SPO_OK;
+}
+
+}  // namespace spo

@@ -1,0 +1,388 @@
+// spo_eval.cu -- fused V / VGL / VGH gather-contract kernels for sm_100a.
+//
+// Reference: kernels.py:132-247 (_prep + _v_soa/_vgl_soa/_vgh_soa) and the
+// batch drivers kernels.py:357-381; dispatch kernels.py:445-473.
+//
+// One CTA = (a block of `ppc` positions) x (one orbital chunk of one tile).
+// Grid: x = position block (fastest) -> all position blocks of chunk 0 run
+// before chunk 1 (tile-major, the paper's AoSoA cache blocking: one tile
+// slice of the table is the L2 working set at a time).  Threads: blockDim.x =
+// `chv` 16-byte orbital vectors (float4 / double2) along the row, blockDim.y =
+// position groups; each group walks its positions.
+//
+// Prologue (fused): the first `ppc` threads map their position to (i0,j0,k0)
+// and 36 basis weights bit-exactly (spo_prologue.cuh) into shared memory.
+//
+// Contraction, per position and 16-byte lane vector:
+//   FAST   separable: s_b = sum_k wz_b[k] c[k]   (b = 0,1,2 derivative order)
+//                     t_ab += wy_a[j] s_b         (per i, 6 combos for VGH)
+//                     acc  += wx_c[i] t_ab        (10 streams)
+//          = 328 FMA / orbital for VGH (vs 640 mul+add in the reference).
+//   STRICT the reference order i, j, k with fp32 prefactors (a_i*a_j)*a_k and
+//          acc = acc + pre*c as separate round-to-nearest mul and add -- bitwise
+//          equal to the numba kernels (kernels.py:219-247, 189 for `pl`).
+// Loads are 16-byte read-only (ld.global.nc) row reads, coalesced across the
+// warp; stores are 16-byte streaming (st.global.cs) so outputs do not evict
+// the table from L2.
+#include "spo_common.cuh"
+#include "spo_prologue.cuh"
+
+namespace spo {
+
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+    static constexpr int W = 4;
+};
+template <>
+struct Vec<double> {
+    static constexpr int W = 2;
+};
+
+__device__ __forceinline__ void ld16(const float *p, float *r) {
+    float4 v = __ldg(reinterpret_cast<const float4 *>(p));
+    r[0] = v.x;
+    r[1] = v.y;
+    r[2] = v.z;
+    r[3] = v.w;
+}
+__device__ __forceinline__ void ld16(const double *p, double *r) {
+    double2 v = __ldg(reinterpret_cast<const double2 *>(p));
+    r[0] = v.x;
+    r[1] = v.y;
+}
+__device__ __forceinline__ void st16(float *p, const float *r) {
+    __stcs(reinterpret_cast<float4 *>(p), make_float4(r[0], r[1], r[2], r[3]));
+}
+__device__ __forceinline__ void st16(double *p, const double *r) {
+    __stcs(reinterpret_cast<double2 *>(p), make_double2(r[0], r[1]));
+}
+__device__ __forceinline__ float fmaT(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fmaT(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+template <int KIND>
+struct Streams {
+    static constexpr int S = KIND == SPO_KIND_V ? 1 : (KIND == SPO_KIND_VGL ? 5 : 10);
+};
+
+struct EvalArgs {
+    const void *table;
+    long long tile_stride;
+    int nb;
+    int chv;              // 16-byte vectors per chunk (= blockDim.x)
+    int chunks_per_tile;  // nb / (chv * W)
+    long long si, sj, sk; // element strides of i', j', k'
+    int nyp, nzp;
+    const double *pos;
+    long long n_pos;
+    int ppc;              // positions per CTA
+    GridArgs g;
+    void *out;
+    long long out_pos_stride, out_stream_stride;
+    const long long *out_index;
+    int *status;
+};
+
+// ---------------------------------------------------------------- FAST ----
+template <int KIND, typename T>
+__device__ __forceinline__ void contract_fast(const T *__restrict__ rp, long long si, long long sj,
+                                              long long sk, const T *__restrict__ w,
+                                              T (&acc)[Streams<KIND>::S][Vec<T>::W]) {
+    constexpr int W = Vec<T>::W;
+    T wx[12], wy[12], wz[12];
+#pragma unroll
+    for (int e = 0; e < 12; ++e) {
+        wx[e] = w[e];
+        wy[e] = w[12 + e];
+        wz[e] = w[24 + e];
+    }
+#pragma unroll
+    for (int s = 0; s < Streams<KIND>::S; ++s)
+#pragma unroll
+        for (int e = 0; e < W; ++e) acc[s][e] = T(0);
+
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        // t_ab: y-derivative order a, z-derivative order b
+        T t00[W], t10[W], t01[W], t20[W], t11[W], t02[W];
+#pragma unroll
+        for (int e = 0; e < W; ++e) t00[e] = t10[e] = t01[e] = t20[e] = t11[e] = t02[e] = T(0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const T *r = rp + i * si + j * sj;
+            T c0[W], c1[W], c2[W], c3[W];
+            ld16(r, c0);
+            ld16(r + sk, c1);
+            ld16(r + 2 * sk, c2);
+            ld16(r + 3 * sk, c3);
+#pragma unroll
+            for (int e = 0; e < W; ++e) {
+                const T s0 = fmaT(wz[3], c3[e], fmaT(wz[2], c2[e], fmaT(wz[1], c1[e], wz[0] * c0[e])));
+                t00[e] = fmaT(wy[j], s0, t00[e]);
+                if (KIND != SPO_KIND_V) {
+                    const T s1 =
+                        fmaT(wz[7], c3[e], fmaT(wz[6], c2[e], fmaT(wz[5], c1[e], wz[4] * c0[e])));
+                    const T s2 =
+                        fmaT(wz[11], c3[e], fmaT(wz[10], c2[e], fmaT(wz[9], c1[e], wz[8] * c0[e])));
+                    t10[e] = fmaT(wy[4 + j], s0, t10[e]);
+                    t01[e] = fmaT(wy[j], s1, t01[e]);
+                    t20[e] = fmaT(wy[8 + j], s0, t20[e]);
+                    t02[e] = fmaT(wy[j], s2, t02[e]);
+                    if (KIND == SPO_KIND_VGH) t11[e] = fmaT(wy[4 + j], s1, t11[e]);
+                }
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < W; ++e) {
+            acc[0][e] = fmaT(wx[i], t00[e], acc[0][e]);
+            if (KIND != SPO_KIND_V) {
+                acc[1][e] = fmaT(wx[4 + i], t00[e], acc[1][e]);  // gx
+                acc[2][e] = fmaT(wx[i], t10[e], acc[2][e]);      // gy
+                acc[3][e] = fmaT(wx[i], t01[e], acc[3][e]);      // gz
+            }
+            if (KIND == SPO_KIND_VGL) {
+                // l = d2x*t00 + x*t20 + x*t02
+                acc[4][e] = fmaT(wx[8 + i], t00[e], fmaT(wx[i], t20[e], fmaT(wx[i], t02[e], acc[4][e])));
+            }
+            if (KIND == SPO_KIND_VGH) {
+                acc[4][e] = fmaT(wx[8 + i], t00[e], acc[4][e]);  // hxx
+                acc[5][e] = fmaT(wx[4 + i], t10[e], acc[5][e]);  // hxy
+                acc[6][e] = fmaT(wx[4 + i], t01[e], acc[6][e]);  // hxz
+                acc[7][e] = fmaT(wx[i], t20[e], acc[7][e]);      // hyy
+                acc[8][e] = fmaT(wx[i], t11[e], acc[8][e]);      // hyz
+                acc[9][e] = fmaT(wx[i], t02[e], acc[9][e]);      // hzz
+            }
+        }
+    }
+}
+
+// -------------------------------------------------------------- STRICT ----
+// kernels.py:219-247 (VGH), 178-196 (VGL), 152-161 (V): fp32, no FMA.
+template <int KIND>
+__device__ __forceinline__ void contract_strict(const float *__restrict__ rp, long long si,
+                                                long long sj, long long sk,
+                                                const float *__restrict__ w,
+                                                float (&acc)[Streams<KIND>::S][4]) {
+    float wx[12], wy[12], wz[12];
+#pragma unroll
+    for (int e = 0; e < 12; ++e) {
+        wx[e] = w[e];
+        wy[e] = w[12 + e];
+        wz[e] = w[24 + e];
+    }
+#pragma unroll
+    for (int s = 0; s < Streams<KIND>::S; ++s)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[s][e] = 0.0f;
+#define MUL3(a, b, c) __fmul_rn(__fmul_rn((a), (b)), (c))
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float c[4];
+                ld16(rp + i * si + j * sj + k * sk, c);
+                const float ax = wx[i], dax = wx[4 + i], d2ax = wx[8 + i];
+                const float ay = wy[j], day = wy[4 + j], d2ay = wy[8 + j];
+                const float az = wz[k], daz = wz[4 + k], d2az = wz[8 + k];
+                float pre[Streams<KIND>::S];
+                pre[0] = MUL3(ax, ay, az);
+                if (KIND != SPO_KIND_V) {
+                    pre[1] = MUL3(dax, ay, az);
+                    pre[2] = MUL3(ax, day, az);
+                    pre[3] = MUL3(ax, ay, daz);
+                }
+                if (KIND == SPO_KIND_VGL) {
+                    // kernels.py:189: d2ax*ay*az + ax*d2ay*az + ax*ay*d2az
+                    pre[4] = __fadd_rn(__fadd_rn(MUL3(d2ax, ay, az), MUL3(ax, d2ay, az)),
+                                       MUL3(ax, ay, d2az));
+                }
+                if (KIND == SPO_KIND_VGH) {
+                    pre[4] = MUL3(d2ax, ay, az);
+                    pre[5] = MUL3(dax, day, az);
+                    pre[6] = MUL3(dax, ay, daz);
+                    pre[7] = MUL3(ax, d2ay, az);
+                    pre[8] = MUL3(ax, day, daz);
+                    pre[9] = MUL3(ax, ay, d2az);
+                }
+#pragma unroll
+                for (int s = 0; s < Streams<KIND>::S; ++s)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[s][e] = __fadd_rn(acc[s][e], __fmul_rn(pre[s], c[e]));
+            }
+        }
+    }
+#undef MUL3
+}
+
+// -------------------------------------------------------------- kernel ----
+template <int KIND, typename T, bool STRICT>
+__global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
+    constexpr int W = Vec<T>::W;
+    constexpr int S = Streams<KIND>::S;
+    extern __shared__ __align__(16) unsigned char smem[];
+    T *sw = reinterpret_cast<T *>(smem);                                  // [ppc][36]
+    long long *sbase = reinterpret_cast<long long *>(sw + a.ppc * 36);    // [ppc]
+
+    const int nthr = blockDim.x * blockDim.y;
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    const long long p0 = (long long)blockIdx.x * a.ppc;
+    const int np = (int)min((long long)a.ppc, a.n_pos - p0);
+
+    for (int q = tid; q < np; q += nthr) {
+        const double *r = a.pos + 3 * (p0 + q);
+        const double x = r[0], y = r[1], z = r[2];
+        double tx, ty, tz;
+        const int i0 = map_axis(x, a.g.dinv[0], a.g.cnt[0], &tx);
+        const int j0 = map_axis(y, a.g.dinv[1], a.g.cnt[1], &ty);
+        const int k0 = map_axis(z, a.g.dinv[2], a.g.cnt[2], &tz);
+        axis_weights<T>(tx, a.g.dinv[0], a.g.delta[0], sw + q * 36);
+        axis_weights<T>(ty, a.g.dinv[1], a.g.delta[1], sw + q * 36 + 12);
+        axis_weights<T>(tz, a.g.dinv[2], a.g.delta[2], sw + q * 36 + 24);
+        const bool finite = isfinite(x) && isfinite(y) && isfinite(z);
+        sbase[q] = finite ? ((long long)i0 * a.nyp + j0) * a.nzp * a.nb + (long long)k0 * a.nb : -1;
+        if (!finite && a.status) atomicOr(a.status, 1);
+    }
+    __syncthreads();
+
+    const int m = blockIdx.y / a.chunks_per_tile;
+    const int c = blockIdx.y - m * a.chunks_per_tile;
+    const int vlane = c * a.chv + threadIdx.x;
+    const T *tb = reinterpret_cast<const T *>(a.table) + (long long)m * a.tile_stride + (long long)vlane * W;
+    const long long lane0 = (long long)m * a.nb + (long long)vlane * W;
+
+    for (int q = threadIdx.y; q < np; q += blockDim.y) {
+        const long long base = sbase[q];
+        T acc[S][W];
+        if (base >= 0) {
+            if constexpr (STRICT) {
+                contract_strict<KIND>(tb + base, a.si, a.sj, a.sk, sw + q * 36, acc);
+            } else {
+                contract_fast<KIND, T>(tb + base, a.si, a.sj, a.sk, sw + q * 36, acc);
+            }
+        } else {
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int e = 0; e < W; ++e) acc[s][e] = T(NAN);
+        }
+        const long long op = a.out_index ? a.out_index[p0 + q] : p0 + q;
+        T *o = reinterpret_cast<T *>(a.out) + op * a.out_pos_stride + lane0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) st16(o + s * a.out_stream_stride, acc[s]);
+    }
+}
+
+template <int KIND, typename T, bool STRICT>
+static int launch(const EvalArgs &a, dim3 grid, dim3 block, size_t smem, cudaStream_t st) {
+    eval_kernel<KIND, T, STRICT><<<grid, block, smem, st>>>(a);
+    return check_launch("spo_eval launch");
+}
+
+}  // namespace spo
+
+using namespace spo;
+
+extern "C" int spo_abi_version(void) { return SPO_ABI_VERSION; }
+
+extern "C" const char *spo_last_error(void) { return last_error_slot().c_str(); }
+
+extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const int32_t *n3,
+                        int32_t nb, int32_t n_tiles, const double *dinv3, const double *delta3,
+                        const double *pos, int64_t n_pos, void *out, int64_t out_pos_stride,
+                        int64_t out_stream_stride, const int64_t *out_index, int32_t *status,
+                        void *stream) {
+    if (kind < SPO_KIND_V || kind > SPO_KIND_VGH) return fail(SPO_ERR_CONTRACT, "unknown kind %d", kind);
+    if (dtype != SPO_F32 && dtype != SPO_F64) return fail(SPO_ERR_CONTRACT, "unknown dtype %d", dtype);
+    if (mode != SPO_MODE_FAST && mode != SPO_MODE_STRICT) return fail(SPO_ERR_CONTRACT, "unknown mode %d", mode);
+    if (mode == SPO_MODE_STRICT && dtype != SPO_F32)
+        return fail(SPO_ERR_CONFIG, "strict mode reproduces the fp32 reference kernels only");
+    TableGeom geo;
+    int rc = make_geom(n3, nb, n_tiles, dtype, &geo);
+    if (rc) return rc;
+    if (n_pos < 0) return fail(SPO_ERR_CONTRACT, "n_pos=%lld < 0", (long long)n_pos);
+    if (n_pos == 0) return ok();
+    if (!table || !pos || !out || !dinv3 || !delta3) return fail(SPO_ERR_CONTRACT, "NULL pointer argument");
+    const int W = dtype == SPO_F64 ? 2 : 4;
+    const int S = kind == SPO_KIND_V ? 1 : (kind == SPO_KIND_VGL ? 5 : 10);
+    if (!aligned16(table) || !aligned16(out))
+        return fail(SPO_ERR_CONTRACT, "table and out must be 16-byte aligned");
+    if (out_pos_stride % W || out_stream_stride % W)
+        return fail(SPO_ERR_CONTRACT, "output strides must be multiples of %d elements", W);
+    const long long lanes = (long long)nb * n_tiles;
+    if (S > 1 && out_stream_stride < lanes)
+        return fail(SPO_ERR_CONTRACT, "out_stream_stride %lld shorter than the %lld table lanes",
+                    (long long)out_stream_stride, lanes);
+    if (out_pos_stride < (long long)(S - 1) * out_stream_stride + lanes && !(n_pos == 1 && !out_index))
+        return fail(SPO_ERR_CONTRACT, "out_pos_stride %lld too small for %d streams",
+                    (long long)out_pos_stride, S);
+    for (int ax = 0; ax < 3; ++ax)
+        if (!(dinv3[ax] > 0.0) || !(delta3[ax] > 0.0))
+            return fail(SPO_ERR_CONFIG, "grid spacing on axis %d must be positive", ax);
+
+    EvalArgs a;
+    a.table = table;
+    a.tile_stride = geo.tile_stride;
+    a.nb = nb;
+    const int Q = nb / W;  // 16-byte vectors per row, multiple of 8
+    int chv = 8;
+    for (int d = 8; d <= 256 && d <= Q; d += 8)
+        if (Q % d == 0) chv = d;
+    a.chv = chv;
+    a.chunks_per_tile = Q / chv;
+    a.sk = nb;
+    a.sj = (long long)geo.nzp * nb;
+    a.si = (long long)geo.nyp * geo.nzp * nb;
+    a.nyp = geo.nyp;
+    a.nzp = geo.nzp;
+    a.pos = pos;
+    a.n_pos = n_pos;
+    for (int ax = 0; ax < 3; ++ax) {
+        a.g.dinv[ax] = dinv3[ax];
+        a.g.cnt[ax] = (double)n3[ax];
+        a.g.delta[ax] = delta3[ax];
+        a.g.n[ax] = n3[ax];
+    }
+    a.out = out;
+    a.out_pos_stride = out_pos_stride;
+    a.out_stream_stride = out_stream_stride;
+    a.out_index = reinterpret_cast<const long long *>(out_index);
+    a.status = status;
+
+    const int groups = 256 / chv;
+    const long long n_chunks = (long long)a.chunks_per_tile * n_tiles;
+    if (n_chunks > 65535) return fail(SPO_ERR_CONFIG, "too many orbital chunks (%lld)", n_chunks);
+    // positions per CTA: up to 4 per group while keeping >= 4 CTAs per SM
+    int ppg = 4;
+    while (ppg > 1 && ((n_pos + (long long)groups * ppg - 1) / ((long long)groups * ppg)) * n_chunks < 4 * 148)
+        ppg >>= 1;
+    a.ppc = groups * ppg;
+    const long long nblk = (n_pos + a.ppc - 1) / a.ppc;
+    if (nblk > 0x7fffffffLL) return fail(SPO_ERR_CONFIG, "too many positions");
+    dim3 grid((unsigned)nblk, (unsigned)n_chunks);
+    dim3 block(chv, groups);
+    const size_t smem = (size_t)a.ppc * (36 * (size_t)(dtype == SPO_F64 ? 8 : 4) + 8);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+
+    if (dtype == SPO_F64) {
+        switch (kind) {
+            case SPO_KIND_V: return launch<SPO_KIND_V, double, false>(a, grid, block, smem, st);
+            case SPO_KIND_VGL: return launch<SPO_KIND_VGL, double, false>(a, grid, block, smem, st);
+            default: return launch<SPO_KIND_VGH, double, false>(a, grid, block, smem, st);
+        }
+    }
+    if (mode == SPO_MODE_STRICT) {
+        switch (kind) {
+            case SPO_KIND_V: return launch<SPO_KIND_V, float, true>(a, grid, block, smem, st);
+            case SPO_KIND_VGL: return launch<SPO_KIND_VGL, float, true>(a, grid, block, smem, st);
+            default: return launch<SPO_KIND_VGH, float, true>(a, grid, block, smem, st);
+        }
+    }
+    switch (kind) {
+        case SPO_KIND_V: return launch<SPO_KIND_V, float, false>(a, grid, block, smem, st);
+        case SPO_KIND_VGL: return launch<SPO_KIND_VGL, float, false>(a, grid, block, smem, st);
+        default: return launch<SPO_KIND_VGH, float, false>(a, grid, block, smem, st);
+    }
+}

@@ -1,0 +1,199 @@
+// spo_table.cu -- device table construction in the wrap-padded AoSoA layout.
+//
+//   spo_pack_table      reference SoA (coeffs.py:117-138) -> device layout,
+//                       optionally split into tiles (coeffs.py:197-210)
+//   spo_fill_uniform    FillSpec.random (coeffs.py:91-94) bit-identically:
+//                       numpy's Philox4x64-10 bit generator (counter 0, key from
+//                       SeedSequence(entropy=seed, spawn_key=(n,))), float32
+//                       draw = (u32 >> 8) * 2^-24, then *2 - 1 in fp32
+//   spo_fill_normal_f64 builder-defined Box-Muller N(0,1) on the same streams
+//
+// Every kernel walks the destination in its own layout (row-major over
+// (m, i', j', k', l)) so stores are fully coalesced; each element finds its
+// reference element (i'-1 mod nx, ...) and spline m*tile_size + l.
+#include "spo_common.cuh"
+
+namespace spo {
+
+struct PackGeom {
+    int nx, ny, nz, nxp, nyp, nzp, nb, tile_size, n_splines;
+    long long total;  // elements in the destination
+};
+
+__device__ __forceinline__ bool dst_coords(const PackGeom &g, long long e, int *n, long long *ref_flat) {
+    const int l = (int)(e % g.nb);
+    long long r = e / g.nb;
+    const int kp = (int)(r % g.nzp);
+    r /= g.nzp;
+    const int jp = (int)(r % g.nyp);
+    r /= g.nyp;
+    const int ip = (int)(r % g.nxp);
+    const int m = (int)(r / g.nxp);
+    const int spl = m * g.tile_size + l;
+    if (l >= g.tile_size || spl >= g.n_splines) return false;
+    const int ii = (ip + g.nx - 1) % g.nx, jj = (jp + g.ny - 1) % g.ny, kk = (kp + g.nz - 1) % g.nz;
+    *n = spl;
+    *ref_flat = ((long long)ii * g.ny + jj) * g.nz + kk;
+    return true;
+}
+
+template <typename T>
+__global__ void pack_kernel(const T *__restrict__ src, int src_npad, PackGeom g, T *__restrict__ dst) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < g.total;
+         e += (long long)gridDim.x * blockDim.x) {
+        int n;
+        long long f;
+        dst[e] = dst_coords(g, e, &n, &f) ? src[f * src_npad + n] : T(0);
+    }
+}
+
+// ---- numpy Philox4x64-10 (numpy/random/src/philox/philox.h) -------------
+struct U4 {
+    unsigned long long v[4];
+};
+
+__device__ __forceinline__ U4 philox4x64_10(U4 c, unsigned long long k0, unsigned long long k1) {
+    const unsigned long long M0 = 0xD2E7470EE14C6C93ULL, M1 = 0xCA5A826395121157ULL;
+    const unsigned long long W0 = 0x9E3779B97F4A7C15ULL, W1 = 0xBB67AE8584CAA73BULL;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += W0;
+            k1 += W1;
+        }
+        const unsigned long long hi0 = __umul64hi(M0, c.v[0]), lo0 = M0 * c.v[0];
+        const unsigned long long hi1 = __umul64hi(M1, c.v[2]), lo1 = M1 * c.v[2];
+        U4 o;
+        o.v[0] = hi1 ^ c.v[1] ^ k0;
+        o.v[1] = lo1;
+        o.v[2] = hi0 ^ c.v[3] ^ k1;
+        o.v[3] = lo0;
+        c = o;
+    }
+    return c;
+}
+
+// 64-bit word w of a stream whose counter starts at 0 (incremented before
+// each 4-word block): block w/4 uses counter w/4 + 1.
+__device__ __forceinline__ unsigned long long philox_word(unsigned long long w, unsigned long long k0,
+                                                          unsigned long long k1) {
+    U4 c;
+    const unsigned long long b = (w >> 2) + 1ULL;
+    c.v[0] = b;
+    c.v[1] = (b == 0ULL) ? 1ULL : 0ULL;  // carry (never reached in practice)
+    c.v[2] = 0ULL;
+    c.v[3] = 0ULL;
+    const U4 o = philox4x64_10(c, k0, k1);
+    return o.v[w & 3];
+}
+
+__global__ void fill_uniform_kernel(const unsigned long long *__restrict__ keys, PackGeom g,
+                                    float *__restrict__ dst) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < g.total;
+         e += (long long)gridDim.x * blockDim.x) {
+        int n;
+        long long f;
+        float v = 0.0f;
+        if (dst_coords(g, e, &n, &f)) {
+            // next_uint32: low half of word f/2 first, then its high half
+            const unsigned long long w = philox_word((unsigned long long)f >> 1, keys[2 * n], keys[2 * n + 1]);
+            const unsigned int u = (f & 1) ? (unsigned int)(w >> 32) : (unsigned int)(w & 0xffffffffULL);
+            const float r = (float)(u >> 8) * (1.0f / 16777216.0f);
+            v = __fsub_rn(__fmul_rn(r, 2.0f), 1.0f);
+        }
+        dst[e] = v;
+    }
+}
+
+__global__ void fill_normal_kernel(const unsigned long long *__restrict__ keys, PackGeom g,
+                                   double *__restrict__ dst) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < g.total;
+         e += (long long)gridDim.x * blockDim.x) {
+        int n;
+        long long f;
+        double v = 0.0;
+        if (dst_coords(g, e, &n, &f)) {
+            const unsigned long long k0 = keys[2 * n], k1 = keys[2 * n + 1];
+            const unsigned long long w0 = philox_word(2ULL * f, k0, k1);
+            const unsigned long long w1 = philox_word(2ULL * f + 1ULL, k0, k1);
+            const double u0 = (double)(w0 >> 11) * (1.0 / 9007199254740992.0);
+            const double u1 = (double)(w1 >> 11) * (1.0 / 9007199254740992.0);
+            v = sqrt(-2.0 * log1p(-u0)) * cospi(2.0 * u1);
+        }
+        dst[e] = v;
+    }
+}
+
+static int make_pack_geom(int dtype, int32_t n_splines, const int32_t *n3, int32_t tile_size,
+                          int32_t nb, int32_t n_tiles, PackGeom *g) {
+    TableGeom t;
+    int rc = make_geom(n3, nb, n_tiles, dtype, &t);
+    if (rc) return rc;
+    if (n_splines < 1) return fail(SPO_ERR_CONFIG, "n_splines=%d must be >= 1", n_splines);
+    if (tile_size < 1 || tile_size > nb)
+        return fail(SPO_ERR_CONFIG, "tile_size=%d must be in [1, nb=%d]", tile_size, nb);
+    if ((long long)tile_size * n_tiles < n_splines)
+        return fail(SPO_ERR_CONFIG, "%d tiles of %d splines cannot hold %d splines", n_tiles,
+                    tile_size, n_splines);
+    g->nx = t.nx;
+    g->ny = t.ny;
+    g->nz = t.nz;
+    g->nxp = t.nxp;
+    g->nyp = t.nyp;
+    g->nzp = t.nzp;
+    g->nb = nb;
+    g->tile_size = tile_size;
+    g->n_splines = n_splines;
+    g->total = t.tile_stride * n_tiles;
+    return SPO_OK;
+}
+
+static unsigned grid_for(long long total) {
+    long long b = (total + 255) / 256;
+    return (unsigned)(b < 148LL * 64 ? (b < 1 ? 1 : b) : 148LL * 64);
+}
+
+}  // namespace spo
+
+using namespace spo;
+
+extern "C" int spo_pack_table(int dtype, const void *src, int32_t src_npad, int32_t n_splines,
+                              const int32_t *n3, int32_t tile_size, int32_t nb, int32_t n_tiles,
+                              void *dst, void *stream) {
+    if (dtype != SPO_F32 && dtype != SPO_F64) return fail(SPO_ERR_CONTRACT, "unknown dtype %d", dtype);
+    PackGeom g;
+    int rc = make_pack_geom(dtype, n_splines, n3, tile_size, nb, n_tiles, &g);
+    if (rc) return rc;
+    if (!src || !dst) return fail(SPO_ERR_CONTRACT, "NULL table pointer");
+    if (src_npad < n_splines) return fail(SPO_ERR_CONTRACT, "src_npad=%d < n_splines=%d", src_npad, n_splines);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == SPO_F64)
+        pack_kernel<double><<<grid_for(g.total), 256, 0, st>>>((const double *)src, src_npad, g, (double *)dst);
+    else
+        pack_kernel<float><<<grid_for(g.total), 256, 0, st>>>((const float *)src, src_npad, g, (float *)dst);
+    return check_launch("spo_pack_table");
+}
+
+extern "C" int spo_fill_uniform(const uint64_t *keys, int32_t n_splines, const int32_t *n3,
+                                int32_t tile_size, int32_t nb, int32_t n_tiles, float *dst,
+                                void *stream) {
+    PackGeom g;
+    int rc = make_pack_geom(SPO_F32, n_splines, n3, tile_size, nb, n_tiles, &g);
+    if (rc) return rc;
+    if (!keys || !dst) return fail(SPO_ERR_CONTRACT, "NULL pointer");
+    fill_uniform_kernel<<<grid_for(g.total), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const unsigned long long *>(keys), g, dst);
+    return check_launch("spo_fill_uniform");
+}
+
+extern "C" int spo_fill_normal_f64(const uint64_t *keys, int32_t n_splines, const int32_t *n3,
+                                   int32_t tile_size, int32_t nb, int32_t n_tiles, double *dst,
+                                   void *stream) {
+    PackGeom g;
+    int rc = make_pack_geom(SPO_F64, n_splines, n3, tile_size, nb, n_tiles, &g);
+    if (rc) return rc;
+    if (!keys || !dst) return fail(SPO_ERR_CONTRACT, "NULL pointer");
+    fill_normal_kernel<<<grid_for(g.total), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const unsigned long long *>(keys), g, dst);
+    return check_launch("spo_fill_normal_f64");
+}

@@ -1,0 +1,405 @@
+"""V / VGL / VGH evaluation: the drop-in surface and the batched device API.
+
+Drop-in (same names, signatures, errors and output semantics as the
+reference kernels.py):
+    KernelKind, WalkerOutputsSoA, WalkerOutputsAoS, eval_batch, eval_v,
+    eval_vgl, eval_vgh, eval_tiled, allocate_outputs, collect_streams.
+  ``eval_batch(table, kind, positions, out)`` evaluates every position on the
+  GPU and -- like kernels.py:353-354 -- leaves the LAST position's streams in
+  the caller's host buffers.
+
+Batched (the north-star entry points):
+    evaluate(table, kind, positions, out=None, mode="fast") -> [P][S][lanes]
+    evaluate_v / evaluate_vgl / evaluate_vgh(table, positions, ...)
+  positions: (P, 3) float64 (device tensor, or host array -> copied), output
+  a CUDA tensor with one block of S streams per position (reference stream
+  order, kernels.py:46-51); ``streams(...)`` turns it into {name: [P, N]}.
+
+There is no CPU path: everything below calls libspo_b200.so (spo_eval).
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+
+import numpy as np
+
+from . import _abi
+from .coeffs import CoeffTableAoS, CoeffTableSoA, TiledCoeffTable, aligned_zeros, padded_count
+from .device import DeviceTable, _resolve_device, _stream_ptr, as_device_table
+from .errors import ContractError, DomainError
+
+
+class KernelKind(enum.Enum):
+    """V = value; VGL = value, gradient, Laplacian; VGH = value, gradient, Hessian
+    (kernels.py:26-51)."""
+
+    V = "v"
+    VGL = "vgl"
+    VGH = "vgh"
+
+    @property
+    def output_streams_soa(self) -> int:
+        return {KernelKind.V: 1, KernelKind.VGL: 5, KernelKind.VGH: 10}[self]
+
+    @property
+    def output_streams_aos(self) -> int:
+        return {KernelKind.V: 1, KernelKind.VGL: 5, KernelKind.VGH: 13}[self]
+
+    def output_streams(self, layout: str) -> int:
+        return self.output_streams_aos if layout == "aos" else self.output_streams_soa
+
+    @property
+    def stream_names(self) -> tuple:
+        if self is KernelKind.V:
+            return ("v",)
+        if self is KernelKind.VGL:
+            return ("v", "gx", "gy", "gz", "l")
+        return ("v", "gx", "gy", "gz", "hxx", "hxy", "hxz", "hyy", "hyz", "hzz")
+
+    @property
+    def code(self) -> int:
+        return {KernelKind.V: _abi.KIND_V, KernelKind.VGL: _abi.KIND_VGL, KernelKind.VGH: _abi.KIND_VGH}[self]
+
+
+def as_kind(kind) -> KernelKind:
+    """Accept our KernelKind, the reference's (bspb.kernels.KernelKind) or a string."""
+    if isinstance(kind, KernelKind):
+        return kind
+    value = getattr(kind, "value", kind)
+    try:
+        return KernelKind(str(value).lower())
+    except ValueError:
+        raise ContractError(f"unknown kernel kind {kind!r}") from None
+
+
+class WalkerOutputsSoA:
+    """Planar output streams v, g[3], l, h[6] of n_padded lanes (kernels.py:54-88)."""
+
+    layout = "soa"
+
+    def __init__(self, n_splines: int):
+        npad = padded_count(n_splines)
+        self.n_splines = n_splines
+        self.n_padded = npad
+        self.v = aligned_zeros(npad)
+        self.g = aligned_zeros((3, npad))
+        self.l = aligned_zeros(npad)
+        self.h = aligned_zeros((6, npad))
+
+    @property
+    def nbytes(self) -> int:
+        return self.v.nbytes + self.g.nbytes + self.l.nbytes + self.h.nbytes
+
+    def streams(self, kind) -> dict:
+        kind = as_kind(kind)
+        n = self.n_splines
+        out = {"v": self.v[:n]}
+        if kind is KernelKind.V:
+            return out
+        out.update(gx=self.g[0, :n], gy=self.g[1, :n], gz=self.g[2, :n])
+        if kind is KernelKind.VGL:
+            out["l"] = self.l[:n]
+            return out
+        for row, name in enumerate(("hxx", "hxy", "hxz", "hyy", "hyz", "hzz")):
+            out[name] = self.h[row, :n]
+        return out
+
+    def _targets(self, kind):
+        """Host rows receiving streams 0..S-1 in reference order."""
+        kind = as_kind(kind)
+        rows = [self.v]
+        if kind is not KernelKind.V:
+            rows += [self.g[0], self.g[1], self.g[2]]
+            rows += [self.l] if kind is KernelKind.VGL else [self.h[r] for r in range(6)]
+        return rows
+
+
+class WalkerOutputsAoS:
+    """Interleaved buffers v[N], g[3N], l[N], h[9N] (kernels.py:91-124)."""
+
+    layout = "aos"
+
+    def __init__(self, n_splines: int):
+        self.n_splines = n_splines
+        self.v = np.zeros(n_splines, dtype=np.float32)
+        self.g = np.zeros(3 * n_splines, dtype=np.float32)
+        self.l = np.zeros(n_splines, dtype=np.float32)
+        self.h = np.zeros(9 * n_splines, dtype=np.float32)
+
+    @property
+    def nbytes(self) -> int:
+        return self.v.nbytes + self.g.nbytes + self.l.nbytes + self.h.nbytes
+
+    def streams(self, kind) -> dict:
+        kind = as_kind(kind)
+        out = {"v": self.v.copy()}
+        if kind is KernelKind.V:
+            return out
+        g = self.g.reshape(-1, 3)
+        out.update(gx=g[:, 0].copy(), gy=g[:, 1].copy(), gz=g[:, 2].copy())
+        if kind is KernelKind.VGL:
+            out["l"] = self.l.copy()
+            return out
+        h = self.h.reshape(-1, 3, 3)
+        for name, (r, c) in (("hxx", (0, 0)), ("hxy", (0, 1)), ("hxz", (0, 2)),
+                             ("hyy", (1, 1)), ("hyz", (1, 2)), ("hzz", (2, 2))):
+            out[name] = h[:, r, c].copy()
+        return out
+
+    def store(self, kind, block: np.ndarray) -> None:
+        """Scatter one position's [S][N] SoA block into the interleaved
+        buffers; the AoS Hessian stores all nine entries (kernels.py:342-350)."""
+        kind = as_kind(kind)
+        n = self.n_splines
+        self.v[:] = block[0, :n]
+        if kind is KernelKind.V:
+            return
+        g = self.g.reshape(-1, 3)
+        g[:, 0], g[:, 1], g[:, 2] = block[1, :n], block[2, :n], block[3, :n]
+        if kind is KernelKind.VGL:
+            self.l[:] = block[4, :n]
+            return
+        h = self.h.reshape(-1, 3, 3)
+        hxx, hxy, hxz, hyy, hyz, hzz = (block[4 + r, :n] for r in range(6))
+        h[:, 0, 0], h[:, 0, 1], h[:, 0, 2] = hxx, hxy, hxz
+        h[:, 1, 0], h[:, 1, 1], h[:, 1, 2] = hxy, hyy, hyz
+        h[:, 2, 0], h[:, 2, 1], h[:, 2, 2] = hxz, hyz, hzz
+
+
+# ----------------------------------------------------------- batched API --
+
+_MODES = {"fast": _abi.MODE_FAST, "strict": _abi.MODE_STRICT}
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _positions_tensor(positions, device):
+    """(P,3) float64 contiguous CUDA tensor; host input -> copied."""
+    torch = _torch()
+    if isinstance(positions, torch.Tensor):
+        pos = positions
+        if pos.dim() == 1:
+            pos = pos.reshape(1, 3)
+        if pos.dim() != 2 or pos.shape[1] != 3:
+            raise ContractError(f"positions must have shape (ns, 3), got {tuple(pos.shape)}")
+        if pos.device != device or pos.dtype != torch.float64 or not pos.is_contiguous():
+            pos = pos.to(device=device, dtype=torch.float64).contiguous()
+        return pos
+    arr = _as_positions(positions)
+    return torch.from_numpy(arr).to(device)
+
+
+def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=None,
+             status=None, check: bool = True):
+    """Evaluate `kind` at every position; returns out[P][S][lanes] (CUDA).
+
+    table      DeviceTable (or any host table -> uploaded once and cached)
+    positions  (P, 3) float64; any finite value (periodic wrap, grid.py:155-167)
+    out        optional preallocated CUDA tensor [>=P][S][lanes] of the table dtype
+    mode       "fast" (separable FMA) or "strict" (bitwise = reference fp32 kernels)
+    out_index  optional int64 CUDA tensor: position p is written to out[out_index[p]]
+    status     optional int32 CUDA tensor(1): set to 1 on a non-finite position
+    check      raise DomainError for non-finite positions (one sync on status)
+    """
+    torch = _torch()
+    kind = as_kind(kind)
+    dt = as_device_table(table)
+    device = dt.device
+    pos = _positions_tensor(positions, device)
+    P = pos.shape[0]
+    S = kind.output_streams_soa
+    tdt = torch.float64 if dt.dtype == np.float64 else torch.float32
+    if out is None:
+        out = torch.empty((P, S, dt.lanes), dtype=tdt, device=device)
+    else:
+        if out.dtype != tdt or out.device != device:
+            raise ContractError("out must be a CUDA tensor of the table dtype on the table device")
+        if out.dim() != 3 or out.shape[1] != S or out.shape[2] < dt.lanes or out.stride(2) != 1:
+            raise ContractError(f"out must be [P][{S}][>={dt.lanes}] with unit lane stride")
+        if out_index is None and out.shape[0] < P:
+            raise ContractError(f"out holds {out.shape[0]} positions, need {P}")
+    if mode not in _MODES:
+        raise ContractError(f"unknown mode {mode!r}")
+    if mode == "strict" and dt.dtype != np.float32:
+        raise ContractError("strict mode reproduces the fp32 reference kernels only")
+    own_status = status is None and check
+    if own_status:
+        status = torch.zeros(1, dtype=torch.int32, device=device)
+    idx_ptr = None
+    if out_index is not None:
+        if out_index.dtype != torch.int64 or out_index.device != device or out_index.numel() != P:
+            raise ContractError("out_index must be an int64 CUDA tensor with one entry per position")
+        idx_ptr = out_index.contiguous().data_ptr()
+    g = dt.grid
+    _abi.check(_abi.load().spo_eval(
+        kind.code, dt.dtype_code, _MODES[mode], dt.data.data_ptr(), _abi.i32x3(g.counts), dt.nb,
+        dt.n_tiles, _abi.f64x3(g.inverse_spacings), _abi.f64x3(g.spacings), pos.data_ptr(), P,
+        out.data_ptr(), out.stride(0), out.stride(1), idx_ptr,
+        status.data_ptr() if status is not None else None, _stream_ptr(device)))
+    if own_status and int(status.item()) != 0:
+        raise DomainError("positions contain non-finite components")
+    return out
+
+
+def evaluate_v(table, positions, out=None, **kw):
+    return evaluate(table, KernelKind.V, positions, out, **kw)
+
+
+def evaluate_vgl(table, positions, out=None, **kw):
+    return evaluate(table, KernelKind.VGL, positions, out, **kw)
+
+
+def evaluate_vgh(table, positions, out=None, **kw):
+    return evaluate(table, KernelKind.VGH, positions, out, **kw)
+
+
+def streams(result, table, kind) -> dict:
+    """{stream name: [P, N] tensor} from an evaluate() result (tile lanes compacted)."""
+    kind = as_kind(kind)
+    dt = as_device_table(table)
+    if dt.tiled:
+        sel = result.index_select(2, dt.lane_index())
+    else:
+        sel = result[:, :, : dt.n_splines]
+    return {name: sel[:, s] for s, name in enumerate(kind.stream_names)}
+
+
+# ----------------------------------------------------------- drop-in API --
+
+def _check_pair(table, out):
+    """kernels.py:415-431.  A longer SoA output is accepted; only the table's
+    lanes are written (the reference reads past the rows there)."""
+    layout = getattr(table, "layout", None)
+    if layout == "soa" or isinstance(table, CoeffTableSoA):
+        if getattr(out, "layout", None) != "soa":
+            raise ContractError("SoA table requires WalkerOutputsSoA")
+        if out.n_padded < table.n_padded:
+            raise ContractError(
+                f"output streams ({out.n_padded}) shorter than table rows ({table.n_padded})")
+    elif layout == "aos" or isinstance(table, CoeffTableAoS):
+        if getattr(out, "layout", None) != "aos":
+            raise ContractError("AoS table requires WalkerOutputsAoS")
+        if out.n_splines < table.n_splines:
+            raise ContractError(
+                f"output buffers ({out.n_splines}) shorter than n_splines ({table.n_splines})")
+    elif isinstance(table, DeviceTable):
+        pass
+    else:
+        raise ContractError(f"unsupported table type {type(table).__name__} (tiled: eval_tiled)")
+
+
+def _as_positions(pos) -> np.ndarray:
+    """kernels.py:434-442: fp64 C-contiguous (ns, 3); (3,) -> (1, 3)."""
+    arr = np.ascontiguousarray(pos, dtype=np.float64)
+    if arr.ndim == 1:
+        arr = arr.reshape(1, 3) if arr.size == 3 else arr
+    if arr.ndim != 2 or arr.shape[1] != 3:
+        raise ContractError(f"positions must have shape (ns, 3), got {arr.shape}")
+    if not np.isfinite(arr).all():
+        raise DomainError("positions contain non-finite components")
+    return arr
+
+
+# positions per device pass of the drop-in path (bounds its scratch buffer)
+DROPIN_CHUNK = 1 << 16
+
+
+def _eval_last(table, kind, pos: np.ndarray, mode: str):
+    """Evaluate all positions on the device; return the last one's [S][lanes]
+    block on the host (reference batch semantics, kernels.py:353-354)."""
+    torch = _torch()
+    dt = as_device_table(table)
+    S = kind.output_streams_soa
+    P = pos.shape[0]
+    chunk = min(P, DROPIN_CHUNK)
+    tdt = torch.float64 if dt.dtype == np.float64 else torch.float32
+    scratch = torch.empty((chunk, S, dt.lanes), dtype=tdt, device=dt.device)
+    dpos = torch.from_numpy(pos).to(dt.device)
+    last = None
+    for lo in range(0, P, chunk):
+        hi = min(P, lo + chunk)
+        evaluate(dt, kind, dpos[lo:hi], scratch, mode=mode, check=False)
+        last = hi - lo - 1
+    return dt, scratch[last].cpu().numpy()
+
+
+def eval_batch(table, kind, positions, out, *, mode: str = "fast") -> None:
+    """Evaluate at every position in order; `out` keeps the last one
+    (kernels.py:445-473).  Tiled tables take one WalkerOutputsSoA per tile."""
+    kind = as_kind(kind)
+    pos = _as_positions(positions)
+    layout = getattr(table, "layout", None)
+    if layout == "aosoa" or isinstance(table, TiledCoeffTable):
+        if len(out) != table.n_tiles:
+            raise ContractError(f"{len(out)} output sets for {table.n_tiles} tiles")
+        for tile_out in out:
+            if getattr(tile_out, "layout", None) != "soa" or tile_out.n_padded < padded_count(table.tile_size):
+                raise ContractError("tiled tables need one WalkerOutputsSoA of tile_size per tile")
+        if pos.shape[0] == 0:
+            return
+        dt, block = _eval_last(table, kind, pos, mode)
+        for m, tile_out in enumerate(out):
+            width = min(dt.tile_size, dt.n_splines - m * dt.tile_size)
+            for s, row in enumerate(tile_out._targets(kind)):
+                row[:width] = block[s, m * dt.nb: m * dt.nb + width]
+                row[width: padded_count(dt.tile_size)] = 0.0
+        return
+    _check_pair(table, out)
+    if pos.shape[0] == 0:
+        return
+    dt, block = _eval_last(table, kind, pos, mode)
+    if getattr(out, "layout", None) == "aos":
+        out.store(kind, block)
+        return
+    n = dt.n_splines
+    width = min(out.n_padded, dt.lanes)
+    for s, row in enumerate(out._targets(kind)):
+        row[:n] = block[s, :n]
+        row[n:width] = 0.0  # padding lanes stay zero (test_kernels.py:181-187)
+
+
+def eval_v(table, pos, out, **kw) -> None:
+    """value of every spline at one position (kernels.py:476-478)."""
+    eval_batch(table, KernelKind.V, pos, out, **kw)
+
+
+def eval_vgl(table, pos, out, **kw) -> None:
+    """value, gradient and Laplacian (kernels.py:481-483)."""
+    eval_batch(table, KernelKind.VGL, pos, out, **kw)
+
+
+def eval_vgh(table, pos, out, **kw) -> None:
+    """value, gradient and symmetric Hessian (kernels.py:486-488)."""
+    eval_batch(table, KernelKind.VGH, pos, out, **kw)
+
+
+def eval_tiled(tiled, kind, pos, outs, **kw) -> None:
+    """Per-tile evaluation; concatenated outputs equal the untiled ones (kernels.py:491-496)."""
+    if not (getattr(tiled, "layout", None) == "aosoa" or isinstance(tiled, TiledCoeffTable)):
+        raise ContractError("eval_tiled expects a TiledCoeffTable")
+    eval_batch(tiled, kind, pos, outs, **kw)
+
+
+def allocate_outputs(table):
+    """Output buffers matching a table's layout (kernels.py:499-507)."""
+    layout = getattr(table, "layout", None)
+    if layout == "aosoa" or isinstance(table, TiledCoeffTable):
+        return [WalkerOutputsSoA(t.n_splines) for t in table.tiles]
+    if layout == "soa" or isinstance(table, CoeffTableSoA):
+        return WalkerOutputsSoA(table.n_splines)
+    if layout == "aos" or isinstance(table, CoeffTableAoS):
+        return WalkerOutputsAoS(table.n_splines)
+    raise ContractError(f"unsupported table type {type(table).__name__}")
+
+
+def collect_streams(out, kind) -> dict:
+    """{stream name: float32 array of length N}; tile lists concatenated (kernels.py:510-519)."""
+    if isinstance(out, (list, tuple)):
+        parts = [o.streams(kind) for o in out]
+        return {name: np.concatenate([np.asarray(p[name]) for p in parts]) for name in parts[0]}
+    return {name: np.array(arr, copy=True) for name, arr in out.streams(kind).items()}

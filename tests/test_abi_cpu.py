@@ -1,0 +1,84 @@
+"""The C-ABI library loads without a GPU, exports every symbol the header
+declares, and rejects bad arguments with the documented codes before any
+CUDA call is made."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_1611_02665_b200 import _abi
+from paper_1611_02665_b200.errors import ConfigError, ContractError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "spo_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(spo_\w+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    return _abi.load()
+
+
+def test_library_exports_every_header_symbol(lib):
+    syms = header_symbols()
+    assert len(syms) >= 8
+    raw = ctypes.CDLL(_abi.LIB_PATH)
+    for s in syms:
+        assert hasattr(raw, s), s
+    assert set(syms) == set(_abi.EXPORTS)
+
+
+def test_abi_version(lib):
+    assert lib.spo_abi_version() == 1
+
+
+def _eval(lib, **kw):
+    a = dict(kind=2, dtype=0, mode=0, table=16, n3=(16, 16, 16), nb=64, n_tiles=1,
+             dinv=(16.0,) * 3, delta=(1 / 16,) * 3, pos=16, n=10, out=16, ps=640, ss=64)
+    a.update(kw)
+    return lib.spo_eval(a["kind"], a["dtype"], a["mode"], a["table"], _abi.i32x3(a["n3"]), a["nb"],
+                        a["n_tiles"], _abi.f64x3(a["dinv"]), _abi.f64x3(a["delta"]), a["pos"], a["n"],
+                        a["out"], a["ps"], a["ss"], None, None, None)
+
+
+def test_eval_argument_validation(lib):
+    assert _eval(lib, kind=7) == 1
+    assert _eval(lib, dtype=3) == 1
+    assert _eval(lib, mode=5) == 1
+    assert _eval(lib, mode=1, dtype=1, nb=64, ps=640) == 3  # strict is fp32 only
+    assert _eval(lib, nb=48) == 1                             # not a 128-byte row
+    assert _eval(lib, n3=(3, 16, 16)) == 3                     # grid too small
+    assert _eval(lib, table=8) == 1                            # misaligned
+    assert _eval(lib, ss=32) == 1                              # streams overlap lanes
+    assert _eval(lib, ps=320) == 1                             # positions overlap
+    assert _eval(lib, n=0) == 0                                # empty batch: no-op
+    assert _eval(lib, dinv=(0.0, 1.0, 1.0)) == 3
+    assert b"positive" in lib.spo_last_error()
+
+
+def test_error_codes_map_to_reference_exceptions(lib):
+    _eval(lib, kind=7)
+    with pytest.raises(ContractError):
+        _abi.check(1)
+    with pytest.raises(ConfigError):
+        _abi.check(3)
+
+
+def test_pack_and_fill_validation(lib):
+    n3 = _abi.i32x3((8, 8, 8))
+    assert lib.spo_pack_table(0, 16, 16, 16, n3, 16, 30, 1, 16, None) == 1   # nb not 128 B
+    assert lib.spo_pack_table(0, 16, 16, 64, n3, 16, 32, 2, 16, None) == 3   # tiles too small
+    assert lib.spo_fill_uniform(16, 0, n3, 16, 32, 1, 16, None) == 3
+    assert lib.spo_fill_normal_f64(16, 16, n3, 16, 8, 1, 16, None) == 1     # nb not 128 B
+
+
+def test_oracle_library_builds_and_loads():
+    import oracle
+
+    L = oracle.lib()
+    assert L.orc_abi_version() == 1
