@@ -46,7 +46,7 @@ UNIT = "orbital-evals/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--config", type=int, default=4)
@@ -102,7 +102,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -112,10 +112,17 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, t0=None, t1=None):
+        """Median SM clock and active throttle reasons over samples taken in
+        [t0, t1] (the timed region), falling back to all samples under load."""
         sm, mx, reasons = [], 0.0, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        lines = [ln for ts, ln in self.lines if t0 is None or t0 - 0.25 <= ts <= t1 + 0.25]
+        window = "timed region"
+        if len(lines) < 2:
+            lines = [ln for _, ln in self.lines]
+            window = "warm-up + timed region"
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -130,7 +137,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": window}
 
 
 def workload(args, rank):
@@ -277,20 +284,21 @@ def run_b200(args):
     evaluate(table, kind, pos[:chunk], out, mode=args.mode, status=status, check=False)
     assert int(status.item()) == 0
 
-    for _ in range(args.warmup):
-        step()
-    barrier()
     launch_events = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                       for _ in bounds] for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
+        for _ in range(args.warmup):
+            step()
         barrier()
+        wall0 = time.time()
         t_start.record(stream)
         for k in range(args.steps):
             step(launch_events[k])
         t_end.record(stream)
         barrier()
+        wall1 = time.time()
     elapsed_ms = t_start.elapsed_time(t_end)
     launch_ms = [s.elapsed_time(e) for ev in launch_events for (s, e) in ev]
     full = [ms for (lo, hi), ms in zip(bounds * args.steps, launch_ms) if hi - lo == chunk]
@@ -307,7 +315,7 @@ def run_b200(args):
     value = total_units / (elapsed_ms / 1e3)
 
     peak, peak_src = measured_peak()
-    achieved = bpp * chunk / (avg_launch_ms / 1e-3) / 1e9  # GB/s per launch
+    achieved = bpp * chunk / (avg_launch_ms * 1e-3) / 1e9  # GB/s per launch
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(args, cfg, kind, chunk),
                 "peak_source": peak_src, "kernel": f"spo::eval_kernel<{kind.upper()},float,{args.mode}>",
@@ -329,7 +337,7 @@ def run_b200(args):
                    "parallelism": f"walker-sharded x{world}, table replicated"},
         "roofline": roofline,
         "gpu_launches": len(bounds) * args.steps,
-        "clocks": clocks.summary(),
+        "clocks": clocks.summary(wall0, wall1),
     }
 
     if rank == 0 and not args.no_e2e:
