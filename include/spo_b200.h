@@ -58,7 +58,7 @@
 extern "C" {
 #endif
 
-#define SPO_ABI_VERSION 1
+#define SPO_ABI_VERSION 2
 
 /* kernel kinds: KernelKind (kernels.py:26-51) */
 #define SPO_KIND_V 0
@@ -92,11 +92,21 @@ const char *spo_last_error(void);
  *   status  device int32 or NULL: OR-ed with 1 when a position is non-finite
  *           (that position's outputs are NaN), so callers can raise DomainError
  *           without a synchronising pre-check.
+ *   workspace, workspace_bytes
+ *           device scratch owned by the caller, at least
+ *           spo_eval_workspace_bytes(kind, dtype, mode, n_pos) bytes, 16-byte
+ *           aligned, not shared with a concurrent call.  With it, fp32 FAST
+ *           calls run the TMA-pipelined kernel (per-position records + a work
+ *           ticket); with NULL they run the generic kernel.  Same results.
  */
 int spo_eval(int kind, int dtype, int mode, const void *table, const int32_t *n3, int32_t nb,
              int32_t n_tiles, const double *dinv3, const double *delta3, const double *pos,
              int64_t n_pos, void *out, int64_t out_pos_stride, int64_t out_stream_stride,
-             const int64_t *out_index, int32_t *status, void *stream);
+             const int64_t *out_index, int32_t *status, void *workspace, int64_t workspace_bytes,
+             void *stream);
+
+/* Workspace spo_eval wants for this request (0 = none used, -1 = bad args). */
+int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64_t n_pos);
 
 /*
  * Per-position prologue: idx [n_pos][3] int32 (i0, j0, k0), t [n_pos][3]

@@ -18,8 +18,10 @@ LIB_PATH = os.path.join(_PKG, "libspo_b200.so")
 KIND_V, KIND_VGL, KIND_VGH = 0, 1, 2
 F32, F64 = 0, 1
 MODE_FAST, MODE_STRICT = 0, 1
+ABI_VERSION = 2
 
-EXPORTS = ("spo_abi_version", "spo_last_error", "spo_eval", "spo_prologue", "spo_basis_weights",
+EXPORTS = ("spo_abi_version", "spo_last_error", "spo_eval", "spo_eval_workspace_bytes", "spo_prologue",
+           "spo_basis_weights",
            "spo_pack_table",
            "spo_fill_uniform", "spo_fill_normal_f64")
 
@@ -51,7 +53,9 @@ def load(build_if_missing: bool = True):
         L.spo_last_error.restype = ctypes.c_char_p
         L.spo_eval.restype = ip
         L.spo_eval.argtypes = [ip, ip, ip, vp, P(i32), i32, i32, P(dbl), P(dbl), vp, i64, vp, i64,
-                               i64, vp, vp, vp]
+                               i64, vp, vp, vp, i64, vp]
+        L.spo_eval_workspace_bytes.restype = i64
+        L.spo_eval_workspace_bytes.argtypes = [ip, ip, ip, i64]
         L.spo_prologue.restype = ip
         L.spo_prologue.argtypes = [ip, P(i32), P(dbl), P(dbl), vp, i64, vp, vp, vp, vp]
         L.spo_basis_weights.restype = ip
@@ -62,7 +66,7 @@ def load(build_if_missing: bool = True):
         L.spo_fill_uniform.argtypes = [vp, i32, P(i32), i32, i32, i32, vp, vp]
         L.spo_fill_normal_f64.restype = ip
         L.spo_fill_normal_f64.argtypes = [vp, i32, P(i32), i32, i32, i32, vp, vp]
-        if L.spo_abi_version() != 1:
+        if L.spo_abi_version() != ABI_VERSION:
             raise RuntimeError("libspo_b200.so ABI version mismatch; rebuild")
         _lib = L
         return L

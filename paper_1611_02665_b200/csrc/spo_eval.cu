@@ -27,6 +27,8 @@
 #include "spo_common.cuh"
 #include "spo_prologue.cuh"
 
+#include <cstdlib>
+
 namespace spo {
 
 template <typename T>
@@ -218,8 +220,8 @@ __device__ __forceinline__ void contract_strict(const float *__restrict__ rp, lo
 }
 
 // -------------------------------------------------------------- kernel ----
-template <int KIND, typename T, bool STRICT>
-__global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
+template <int KIND, typename T, bool STRICT, int MINB>
+__global__ void __launch_bounds__(256, MINB) eval_kernel(const EvalArgs a) {
     constexpr int W = Vec<T>::W;
     constexpr int S = Streams<KIND>::S;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -277,11 +279,22 @@ __global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
 
 template <int KIND, typename T, bool STRICT>
 static int launch(const EvalArgs &a, dim3 grid, dim3 block, size_t smem, cudaStream_t st) {
-    eval_kernel<KIND, T, STRICT><<<grid, block, smem, st>>>(a);
+    static const int minb = getenv("SPO_MINB") ? atoi(getenv("SPO_MINB")) : 1;
+    if (minb >= 2)
+        eval_kernel<KIND, T, STRICT, 2><<<grid, block, smem, st>>>(a);
+    else
+        eval_kernel<KIND, T, STRICT, 1><<<grid, block, smem, st>>>(a);
     return check_launch("spo_eval launch");
 }
 
 }  // namespace spo
+
+namespace spo {
+int eval_tma(int kind, const float *table, const TableGeom &geo, const GridArgs &g, const double *pos,
+             long long n_pos, float *out, long long ops, long long oss, const long long *out_index, int *status,
+             void *workspace, long long ws_bytes, cudaStream_t st, int cw_request);
+long long eval_tma_workspace_bytes(long long n_pos);
+}
 
 using namespace spo;
 
@@ -289,11 +302,17 @@ extern "C" int spo_abi_version(void) { return SPO_ABI_VERSION; }
 
 extern "C" const char *spo_last_error(void) { return last_error_slot().c_str(); }
 
+extern "C" int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64_t n_pos) {
+    if (kind < SPO_KIND_V || kind > SPO_KIND_VGH || n_pos < 0) return -1;
+    if (dtype != SPO_F32 || mode != SPO_MODE_FAST) return 0;
+    return eval_tma_workspace_bytes(n_pos);
+}
+
 extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const int32_t *n3,
                         int32_t nb, int32_t n_tiles, const double *dinv3, const double *delta3,
                         const double *pos, int64_t n_pos, void *out, int64_t out_pos_stride,
                         int64_t out_stream_stride, const int64_t *out_index, int32_t *status,
-                        void *stream) {
+                        void *workspace, int64_t workspace_bytes, void *stream) {
     if (kind < SPO_KIND_V || kind > SPO_KIND_VGH) return fail(SPO_ERR_CONTRACT, "unknown kind %d", kind);
     if (dtype != SPO_F32 && dtype != SPO_F64) return fail(SPO_ERR_CONTRACT, "unknown dtype %d", dtype);
     if (mode != SPO_MODE_FAST && mode != SPO_MODE_STRICT) return fail(SPO_ERR_CONTRACT, "unknown mode %d", mode);
@@ -321,6 +340,26 @@ extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const 
     for (int ax = 0; ax < 3; ++ax)
         if (!(dinv3[ax] > 0.0) || !(delta3[ax] > 0.0))
             return fail(SPO_ERR_CONFIG, "grid spacing on axis %d must be positive", ax);
+
+    if (dtype == SPO_F32 && mode == SPO_MODE_FAST) {
+        static const char *env_tma = getenv("SPO_TMA");
+        static const char *env_cw = getenv("SPO_CW");
+        if (!(env_tma && env_tma[0] == '0')) {
+            GridArgs g;
+            for (int ax = 0; ax < 3; ++ax) {
+                g.dinv[ax] = dinv3[ax];
+                g.cnt[ax] = (double)n3[ax];
+                g.delta[ax] = delta3[ax];
+                g.n[ax] = n3[ax];
+            }
+            const int r = eval_tma(kind, static_cast<const float *>(table), geo, g, pos, n_pos,
+                                   static_cast<float *>(out), out_pos_stride, out_stream_stride,
+                                   reinterpret_cast<const long long *>(out_index), status, workspace,
+                                   workspace_bytes, reinterpret_cast<cudaStream_t>(stream),
+                                   env_cw ? atoi(env_cw) : 0);
+            if (r >= 0) return r;
+        }
+    }
 
     EvalArgs a;
     a.table = table;

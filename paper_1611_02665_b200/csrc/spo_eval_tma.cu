@@ -1,0 +1,461 @@
+// spo_eval_tma.cu -- TMA-pipelined fp32 V / VGL / VGH kernel (the fast path).
+//
+// Same math as spo_eval.cu's separable FAST contraction (kernels.py:143-247
+// restated as k-, then j-, then i-sums with FMA), different data movement.
+//
+//  1. prologue_records_kernel: one thread per position maps it to (i0,j0,k0)
+//     and the 36 fp32 basis weights, bit-exactly (spo_prologue.cuh), into a
+//     160-byte record in the caller's workspace.  Once per position per call.
+//  2. eval_tma_kernel: persistent CTAs (one per SM) of 8 warps.  Work items
+//     are (unit u = (tile m, chunk c of CW lanes), batch of BP positions) and
+//     are handed out by a global ticket counter in unit-major order, so at any
+//     moment the whole GPU works on one or two units: the L2 working set is one
+//     CW-wide slice of the table (rows x CW x 4 B, 38.5 MB for 67^3 at CW = 32)
+//     -- the paper's AoSoA cache blocking, enforced by scheduling rather than by
+//     hoping CTAs stay in step.
+//     Per warp, a ring of R stages is fed by TMA: one cp.async.bulk.tensor.5d
+//     per (position, i) brings the 4(j) x 4(k) x CW slab (16 rows) into shared
+//     memory and completes on the stage's mbarrier; item records arrive by a
+//     cp.async.bulk copy on their own mbarriers (double-buffered).  The warp
+//     runs R-1 slabs ahead of its compute, across item boundaries.
+//     Compute: lane = (position in group, 16-byte lane vector), 4 orbitals per
+//     lane, S accumulators per orbital kept in registers over the 4 i-slabs,
+//     streaming 16-byte stores.
+#include <cuda.h>
+
+#include "spo_common.cuh"
+#include "spo_prologue.cuh"
+
+namespace spo {
+namespace tma {
+
+constexpr int WARPS = 8;
+constexpr int R = 3;          // ring stages per warp
+constexpr int STAGE = 8192;   // bytes: 128 fp32 lanes x 16 rows
+constexpr int BP = 12;        // positions per work item
+constexpr int REC = 40;       // floats per position record: 36 weights, i0, j0, k0, pad
+constexpr int WS_HEADER = 256;
+
+struct Args {
+    const float *recs;        // [n_pos][REC]
+    unsigned *ticket;
+    long long n_pos;
+    long long nbatch;         // ceil(n_pos / BP)
+    long long n_items;        // units * nbatch
+    int chunks;               // chunks of CW lanes per tile row
+    int nb;                   // table row length (lanes)
+    float *out;
+    long long out_pos_stride, out_stream_stride;
+    const long long *out_index;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, unsigned long long *bar, int c0,
+                                            int c1, int c2, int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "r"(c4)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(src)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int KIND>
+struct NS {
+    static constexpr int S = KIND == SPO_KIND_V ? 1 : (KIND == SPO_KIND_VGL ? 5 : 10);
+};
+
+// One i-slab of the separable contraction for one 16-byte lane vector.
+// slab: [j][k][CW] floats of this lane's position; wy/wz: 12 weights each;
+// ax/dax/d2ax: the x weights of this i.
+template <int KIND, int CW>
+__device__ __forceinline__ void slab_fma(const float *__restrict__ slab, const float (&wy)[12],
+                                         const float (&wz)[12], float ax, float dax, float d2ax,
+                                         float (&acc)[NS<KIND>::S][4]) {
+    float t00[4], t10[4], t01[4], t20[4], t11[4], t02[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) t00[e] = t10[e] = t01[e] = t20[e] = t11[e] = t02[e] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float4 c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const float4 *>(slab + (j * 4 + k) * CW);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float c0 = (&c[0].x)[e], c1 = (&c[1].x)[e], c2 = (&c[2].x)[e], c3 = (&c[3].x)[e];
+            const float s0 = __fmaf_rn(wz[3], c3, __fmaf_rn(wz[2], c2, __fmaf_rn(wz[1], c1, wz[0] * c0)));
+            t00[e] = __fmaf_rn(wy[j], s0, t00[e]);
+            if (KIND != SPO_KIND_V) {
+                const float s1 = __fmaf_rn(wz[7], c3, __fmaf_rn(wz[6], c2, __fmaf_rn(wz[5], c1, wz[4] * c0)));
+                const float s2 = __fmaf_rn(wz[11], c3, __fmaf_rn(wz[10], c2, __fmaf_rn(wz[9], c1, wz[8] * c0)));
+                t10[e] = __fmaf_rn(wy[4 + j], s0, t10[e]);
+                t01[e] = __fmaf_rn(wy[j], s1, t01[e]);
+                t20[e] = __fmaf_rn(wy[8 + j], s0, t20[e]);
+                t02[e] = __fmaf_rn(wy[j], s2, t02[e]);
+                if (KIND == SPO_KIND_VGH) t11[e] = __fmaf_rn(wy[4 + j], s1, t11[e]);
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        acc[0][e] = __fmaf_rn(ax, t00[e], acc[0][e]);
+        if (KIND != SPO_KIND_V) {
+            acc[1][e] = __fmaf_rn(dax, t00[e], acc[1][e]);
+            acc[2][e] = __fmaf_rn(ax, t10[e], acc[2][e]);
+            acc[3][e] = __fmaf_rn(ax, t01[e], acc[3][e]);
+        }
+        if (KIND == SPO_KIND_VGL)
+            acc[4][e] = __fmaf_rn(d2ax, t00[e], __fmaf_rn(ax, t20[e], __fmaf_rn(ax, t02[e], acc[4][e])));
+        if (KIND == SPO_KIND_VGH) {
+            acc[4][e] = __fmaf_rn(d2ax, t00[e], acc[4][e]);
+            acc[5][e] = __fmaf_rn(dax, t10[e], acc[5][e]);
+            acc[6][e] = __fmaf_rn(dax, t01[e], acc[6][e]);
+            acc[7][e] = __fmaf_rn(ax, t20[e], acc[7][e]);
+            acc[8][e] = __fmaf_rn(ax, t11[e], acc[8][e]);
+            acc[9][e] = __fmaf_rn(ax, t02[e], acc[9][e]);
+        }
+    }
+}
+
+// ------------------------------------------------------------ prologue --
+__global__ void prologue_records_kernel(GridArgs g, const double *__restrict__ pos, long long n,
+                                        float *__restrict__ recs, int *__restrict__ status) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x) {
+        const double x = pos[3 * p], y = pos[3 * p + 1], z = pos[3 * p + 2];
+        double tx, ty, tz;
+        int i0 = map_axis(x, g.dinv[0], g.cnt[0], &tx);
+        const int j0 = map_axis(y, g.dinv[1], g.cnt[1], &ty);
+        const int k0 = map_axis(z, g.dinv[2], g.cnt[2], &tz);
+        float w[REC];
+        weights_f32(tx, g.dinv[0], w);
+        weights_f32(ty, g.dinv[1], w + 12);
+        weights_f32(tz, g.dinv[2], w + 24);
+        if (!(isfinite(x) && isfinite(y) && isfinite(z))) {
+            if (status) atomicOr(status, 1);
+            i0 = -1;
+        }
+        w[36] = __int_as_float(i0);
+        w[37] = __int_as_float(j0);
+        w[38] = __int_as_float(k0);
+        w[39] = 0.0f;
+        float4 *dst = reinterpret_cast<float4 *>(recs + p * REC);
+#pragma unroll
+        for (int e = 0; e < REC / 4; ++e) dst[e] = make_float4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+    }
+}
+
+// -------------------------------------------------------------- kernel --
+struct ItemInfo {
+    long long b0;
+    int nb, m, c, G, valid, pad;
+};
+
+template <int KIND, int CW>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    eval_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Args a) {
+    constexpr int S = NS<KIND>::S;
+    constexpr int PW = 128 / CW;       // positions per warp step
+    constexpr int LPP = CW / 4;        // lanes per position
+    constexpr int SLAB = CW * 16 * 4;  // bytes per (position, i) slab
+    static_assert(PW * SLAB == STAGE, "stage must hold one warp step");
+    static_assert(BP % PW == 0, "items hold whole groups");
+
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char *ring = smem + (size_t)warp * R * STAGE;
+    unsigned long long *bars =
+        reinterpret_cast<unsigned long long *>(smem + (size_t)WARPS * R * STAGE) + warp * (R + 2);
+    unsigned long long *rbar = bars + R;  // record barriers of slots 0/1
+    float *recs = reinterpret_cast<float *>(smem + (size_t)WARPS * R * STAGE + WARPS * (R + 2) * 8) +
+                  warp * 2 * BP * REC;
+    ItemInfo *info = reinterpret_cast<ItemInfo *>(smem + (size_t)WARPS * R * STAGE + WARPS * (R + 2) * 8 +
+                                                  WARPS * 2 * BP * REC * 4) + warp * 2;
+
+    if (lane == 0) {
+        for (int s = 0; s < R + 2; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+
+    // Take a ticket and start the record copy of its item into `slot`.
+    auto fill = [&](int slot) {
+        if (lane == 0) {
+            const unsigned long long k = atomicAdd(a.ticket, 1u);
+            ItemInfo it;
+            it.valid = k < (unsigned long long)a.n_items;
+            if (it.valid) {
+                const long long u = (long long)k / a.nbatch;
+                const long long b = (long long)k - u * a.nbatch;
+                it.m = (int)(u / a.chunks);
+                it.c = (int)(u - (long long)it.m * a.chunks);
+                it.b0 = b * BP;
+                it.nb = (int)min((long long)BP, a.n_pos - it.b0);
+                it.G = (it.nb + PW - 1) / PW;
+                fence_proxy_async();  // generic reads of this slot precede the async write
+                mbar_arrive_expect_tx(&rbar[slot], (unsigned)(it.nb * REC * 4));
+                bulk_load(recs + slot * BP * REC, a.recs + it.b0 * REC, (unsigned)(it.nb * REC * 4), &rbar[slot]);
+            } else {
+                it.b0 = 0;
+                it.nb = it.m = it.c = it.G = 0;
+            }
+            info[slot] = it;
+        }
+        __syncwarp();
+    };
+
+    const int pp = lane / LPP;  // position within a group
+    const int vl = lane % LPP;  // 16-byte lane vector within the CW chunk
+
+    int st_i = 0, st_c = 0;  // issue / consume stage indices (same sequence, R-1 apart)
+    unsigned ph_c = 0;       // consume phase parity of stage st_c
+    unsigned rph0 = 0, rph1 = 0;
+
+    fill(0);
+    fill(1);
+
+    // issue cursor
+    int islot = 0, ig = 0, ii = 0;
+    bool iactive = info[0].valid, iready = false;
+    auto issue_next = [&]() {
+        if (!iactive) return;
+        if (!iready) {  // records of this slot must have landed (cells + weights)
+            mbar_wait(&rbar[islot], islot ? rph1 : rph0);
+            if (islot) rph1 ^= 1; else rph0 ^= 1;
+            iready = true;
+        }
+        __syncwarp();  // every lane is done reading this stage (WAR vs TMA)
+        if (lane == 0) {
+            const ItemInfo it = info[islot];
+            const float *rc = recs + islot * BP * REC;
+            unsigned char *dst = ring + st_i * STAGE;
+            bool ok[PW];
+            unsigned bytes = 0;
+#pragma unroll
+            for (int q = 0; q < PW; ++q) {
+                const int p = ig * PW + q;
+                ok[q] = p < it.nb && __float_as_int(rc[p * REC + 36]) >= 0;
+                bytes += ok[q] ? SLAB : 0;
+            }
+            fence_proxy_async();
+            mbar_arrive_expect_tx(&bars[st_i], bytes);
+#pragma unroll
+            for (int q = 0; q < PW; ++q) {
+                const int p = ig * PW + q;
+                if (ok[q])
+                    tma_load_5d(dst + q * SLAB, &tmap, &bars[st_i], it.c * CW, __float_as_int(rc[p * REC + 38]),
+                                __float_as_int(rc[p * REC + 37]), __float_as_int(rc[p * REC + 36]) + ii, it.m);
+            }
+        }
+        if (++st_i == R) st_i = 0;
+        if (++ii == 4) {
+            ii = 0;
+            if (++ig == info[islot].G) {
+                ig = 0;
+                islot ^= 1;
+                iready = false;
+                iactive = info[islot].valid;
+            }
+        }
+    };
+
+    for (int t = 0; t < R - 1; ++t) issue_next();
+
+    int cslot = 0;
+    while (info[cslot].valid) {
+        const ItemInfo it = info[cslot];
+        const float *rc = recs + cslot * BP * REC;
+        for (int g = 0; g < it.G; ++g) {
+            const int p = g * PW + pp;
+            const float *w = rc + min(p, it.nb - 1) * REC;
+            float wx[12], wy[12], wz[12];
+#pragma unroll
+            for (int e = 0; e < 12; e += 4) {
+                const float4 x4 = *reinterpret_cast<const float4 *>(w + e);
+                const float4 y4 = *reinterpret_cast<const float4 *>(w + 12 + e);
+                const float4 z4 = *reinterpret_cast<const float4 *>(w + 24 + e);
+                wx[e] = x4.x, wx[e + 1] = x4.y, wx[e + 2] = x4.z, wx[e + 3] = x4.w;
+                wy[e] = y4.x, wy[e + 1] = y4.y, wy[e + 2] = y4.z, wy[e + 3] = y4.w;
+                wz[e] = z4.x, wz[e + 1] = z4.y, wz[e + 2] = z4.z, wz[e + 3] = z4.w;
+            }
+            const bool finite = __float_as_int(w[36]) >= 0;
+            float acc[S][4];
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[s][e] = 0.0f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                issue_next();
+                mbar_wait(&bars[st_c], ph_c);
+                const float *slab = reinterpret_cast<const float *>(ring + st_c * STAGE + pp * SLAB) + vl * 4;
+                slab_fma<KIND, CW>(slab, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
+                if (++st_c == R) {
+                    st_c = 0;
+                    ph_c ^= 1;
+                }
+            }
+            if (p < it.nb) {
+                const long long gp = it.b0 + p;
+                const long long op = a.out_index ? a.out_index[gp] : gp;
+                float *o = a.out + op * a.out_pos_stride + (long long)it.m * a.nb + it.c * CW + vl * 4;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const float4 v = finite ? make_float4(acc[s][0], acc[s][1], acc[s][2], acc[s][3])
+                                            : make_float4(NAN, NAN, NAN, NAN);
+                    __stcs(reinterpret_cast<float4 *>(o + s * a.out_stream_stride), v);
+                }
+            }
+        }
+        __syncwarp();
+        fill(cslot);  // the issue cursor has left this slot: refill it with the next ticket
+        cslot ^= 1;
+    }
+}
+
+// ---------------------------------------------------------------- host --
+typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiled get_encode() {
+    static EncodeTiled fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiled>(p);
+    }
+    return fn;
+}
+
+constexpr size_t smem_bytes() {
+    return (size_t)WARPS * R * STAGE + WARPS * (R + 2) * 8 + WARPS * 2 * BP * REC * 4 + WARPS * 2 * sizeof(ItemInfo);
+}
+static_assert(smem_bytes() <= 232448, "shared memory budget");
+
+template <int KIND, int CW>
+static int launch_t(const CUtensorMap &map, const Args &a, int grid, cudaStream_t st) {
+    constexpr size_t sm = smem_bytes();
+    cudaFuncSetAttribute(eval_tma_kernel<KIND, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    eval_tma_kernel<KIND, CW><<<grid, WARPS * 32, sm, st>>>(map, a);
+    return check_launch("spo_eval (tma) launch");
+}
+
+}  // namespace tma
+
+long long eval_tma_workspace_bytes(long long n_pos) { return tma::WS_HEADER + n_pos * tma::REC * 4; }
+
+// Called by spo_eval for fp32 FAST requests with a workspace.  Returns -1
+// when the TMA path cannot be used (the caller then uses the generic kernel).
+int eval_tma(int kind, const float *table, const TableGeom &geo, const GridArgs &g, const double *pos,
+             long long n_pos, float *out, long long ops, long long oss, const long long *out_index, int *status,
+             void *workspace, long long ws_bytes, cudaStream_t st, int cw_request) {
+    using namespace tma;
+    if (!workspace || ws_bytes < eval_tma_workspace_bytes(n_pos) || !aligned16(workspace)) return -1;
+    EncodeTiled encode = get_encode();
+    if (!encode) return -1;
+    // chunk width: working set rows x CW x 4 B <= ~40 MB unless overridden
+    const long long rows = (long long)geo.nxp * geo.nyp * geo.nzp;
+    int cw = cw_request;
+    if (cw == 0) {
+        cw = 32;
+        if (rows * 128 * 4 <= (40LL << 20)) cw = 128;
+        else if (rows * 64 * 4 <= (40LL << 20)) cw = 64;
+    }
+    while (cw > 32 && geo.nb % cw) cw >>= 1;
+    if (cw < 32 || geo.nb % cw) return -1;
+
+    CUtensorMap map;
+    cuuint64_t dims[5] = {(cuuint64_t)geo.nb, (cuuint64_t)geo.nzp, (cuuint64_t)geo.nyp, (cuuint64_t)geo.nxp,
+                          (cuuint64_t)geo.n_tiles};
+    cuuint64_t strides[4] = {(cuuint64_t)geo.nb * 4, (cuuint64_t)geo.nzp * geo.nb * 4,
+                             (cuuint64_t)geo.nyp * geo.nzp * geo.nb * 4, (cuuint64_t)geo.tile_stride * 4};
+    cuuint32_t box[5] = {(cuuint32_t)cw, 4, 4, 1, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float *>(table), dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+
+    unsigned char *ws = static_cast<unsigned char *>(workspace);
+    float *recs = reinterpret_cast<float *>(ws + WS_HEADER);
+    if (cudaMemsetAsync(ws, 0, WS_HEADER, st) != cudaSuccess) return check_launch("workspace reset");
+    {
+        long long blocks = (n_pos + 255) / 256;
+        if (blocks > 148LL * 16) blocks = 148LL * 16;
+        prologue_records_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, recs, status);
+        int rc = check_launch("spo_eval (prologue) launch");
+        if (rc) return rc;
+    }
+
+    Args a;
+    a.recs = recs;
+    a.ticket = reinterpret_cast<unsigned *>(ws);
+    a.n_pos = n_pos;
+    a.nbatch = (n_pos + BP - 1) / BP;
+    a.chunks = geo.nb / cw;
+    a.n_items = a.nbatch * (long long)geo.n_tiles * a.chunks;
+    a.nb = geo.nb;
+    a.out = out;
+    a.out_pos_stride = ops;
+    a.out_stream_stride = oss;
+    a.out_index = out_index;
+    if (a.n_items >= (1LL << 32)) return -1;  // 32-bit ticket counter
+
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long warps_needed = (a.n_items + 1) / 2;
+    int grid = (int)min((long long)sms, (warps_needed + WARPS - 1) / WARPS);
+    if (grid < 1) grid = 1;
+#define SPO_TMA_CASE(K)                                      \
+    switch (cw) {                                           \
+        case 32: return launch_t<K, 32>(map, a, grid, st);  \
+        case 64: return launch_t<K, 64>(map, a, grid, st);  \
+        default: return launch_t<K, 128>(map, a, grid, st); \
+    }
+    if (kind == SPO_KIND_V) SPO_TMA_CASE(SPO_KIND_V)
+    if (kind == SPO_KIND_VGL) SPO_TMA_CASE(SPO_KIND_VGL)
+    SPO_TMA_CASE(SPO_KIND_VGH)
+#undef SPO_TMA_CASE
+}
+
+}  // namespace spo

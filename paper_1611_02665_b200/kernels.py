@@ -195,7 +195,7 @@ def _positions_tensor(positions, device):
 
 
 def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=None,
-             status=None, check: bool = True):
+             status=None, check: bool = True, pipeline: bool = True):
     """Evaluate `kind` at every position; returns out[P][S][lanes] (CUDA).
 
     table      DeviceTable (or any host table -> uploaded once and cached)
@@ -205,6 +205,8 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
     out_index  optional int64 CUDA tensor: position p is written to out[out_index[p]]
     status     optional int32 CUDA tensor(1): set to 1 on a non-finite position
     check      raise DomainError for non-finite positions (one sync on status)
+    pipeline   fp32 fast mode: True = TMA-pipelined kernel (needs a workspace,
+               allocated here), False = the generic kernel (same bits)
     """
     torch = _torch()
     kind = as_kind(kind)
@@ -236,11 +238,15 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
             raise ContractError("out_index must be an int64 CUDA tensor with one entry per position")
         idx_ptr = out_index.contiguous().data_ptr()
     g = dt.grid
-    _abi.check(_abi.load().spo_eval(
+    L = _abi.load()
+    ws_bytes = int(L.spo_eval_workspace_bytes(kind.code, dt.dtype_code, _MODES[mode], P)) if pipeline else 0
+    ws = torch.empty(max(ws_bytes, 0), dtype=torch.uint8, device=device) if ws_bytes > 0 else None
+    _abi.check(L.spo_eval(
         kind.code, dt.dtype_code, _MODES[mode], dt.data.data_ptr(), _abi.i32x3(g.counts), dt.nb,
         dt.n_tiles, _abi.f64x3(g.inverse_spacings), _abi.f64x3(g.spacings), pos.data_ptr(), P,
         out.data_ptr(), out.stride(0), out.stride(1), idx_ptr,
-        status.data_ptr() if status is not None else None, _stream_ptr(device)))
+        status.data_ptr() if status is not None else None,
+        ws.data_ptr() if ws is not None else None, max(ws_bytes, 0), _stream_ptr(device)))
     if own_status and int(status.item()) != 0:
         raise DomainError("positions contain non-finite components")
     return out

@@ -34,7 +34,10 @@ def test_library_exports_every_header_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.spo_abi_version() == 1
+    assert lib.spo_abi_version() == 2
+    assert lib.spo_eval_workspace_bytes(2, 0, 0, 1000) >= 1000 * 160
+    assert lib.spo_eval_workspace_bytes(2, 1, 0, 1000) == 0
+    assert lib.spo_eval_workspace_bytes(9, 0, 0, 1000) == -1
 
 
 def _eval(lib, **kw):
@@ -43,7 +46,7 @@ def _eval(lib, **kw):
     a.update(kw)
     return lib.spo_eval(a["kind"], a["dtype"], a["mode"], a["table"], _abi.i32x3(a["n3"]), a["nb"],
                         a["n_tiles"], _abi.f64x3(a["dinv"]), _abi.f64x3(a["delta"]), a["pos"], a["n"],
-                        a["out"], a["ps"], a["ss"], None, None, None)
+                        a["out"], a["ps"], a["ss"], None, None, None, 0, None)
 
 
 def test_eval_argument_validation(lib):

@@ -159,6 +159,18 @@ def test_value_stream_identical_across_kinds(cfg1, golden_cfg1):
         np.testing.assert_array_equal(vgl[:, 1:4], vgh[:, 1:4])
 
 
+@pytest.mark.parametrize("kind", KINDS)
+def test_pipelined_and_generic_kernels_bitwise_equal(cfg1, golden_cfg1, kind):
+    """The TMA-pipelined and the generic fast kernels run the same FMA
+    sequence per lane: identical bits, tiled or not."""
+    host, dt = cfg1
+    pos = golden_cfg1["positions"]
+    for table in (dt, DeviceTable.from_host(host, tile_size=32)):
+        a = evaluate(table, kind, pos, pipeline=True)
+        b = evaluate(table, kind, pos, pipeline=False)
+        assert bool((a == b).all())
+
+
 def test_laplacian_is_hessian_trace(cfg1, golden_cfg1):
     _, dt = cfg1
     pos = golden_cfg1["positions"]
