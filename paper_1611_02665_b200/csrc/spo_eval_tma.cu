@@ -23,16 +23,15 @@
 //     streaming 16-byte stores.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "spo_common.cuh"
 #include "spo_prologue.cuh"
 
 namespace spo {
 namespace tma {
 
-constexpr int WARPS = 8;
-constexpr int R = 3;          // ring stages per warp
 constexpr int STAGE = 8192;   // bytes: 128 fp32 lanes x 16 rows
-constexpr int BP = 12;        // positions per work item
 constexpr int REC = 40;       // floats per position record: 36 weights, i0, j0, k0, pad
 constexpr int WS_HEADER = 256;
 
@@ -47,6 +46,7 @@ struct Args {
     float *out;
     long long out_pos_stride, out_stream_stride;
     const long long *out_index;
+    int evict_last;           // L2 evict_last hint on table slabs
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -75,13 +75,24 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phas
 }
 
 __device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, unsigned long long *bar, int c0,
-                                            int c1, int c2, int c3, int c4) {
+                                            int c1, int c2, int c3, int c4, unsigned long long policy) {
     asm volatile(
-        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<unsigned long long>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
-        "r"(c4)
+        "r"(c4), "l"(policy)
         : "memory");
+}
+
+// L2 policy for table slabs: keep the current unit's slice resident while the
+// output stream (st.global.cs) passes through.
+__device__ __forceinline__ unsigned long long l2_policy(bool evict_last) {
+    unsigned long long p;
+    if (evict_last)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
 }
 
 __device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
@@ -180,14 +191,23 @@ __global__ void prologue_records_kernel(GridArgs g, const double *__restrict__ p
 }
 
 // -------------------------------------------------------------- kernel --
+// Launch shapes: warps per CTA, ring stages per warp, positions per item.
+template <int WARPS_, int R_, int BP_>
+struct TCfg {
+    static constexpr int WARPS = WARPS_, R = R_, BP = BP_;
+};
+using CfgA = TCfg<8, 3, 12>;   // 8 warps, 2 slabs in flight per warp
+using CfgB = TCfg<12, 2, 8>;   // 12 warps, 1 slab in flight per warp
+
 struct ItemInfo {
     long long b0;
     int nb, m, c, G, valid, pad;
 };
 
-template <int KIND, int CW>
-__global__ void __launch_bounds__(WARPS * 32, 1)
+template <int KIND, int CW, class C>
+__global__ void __launch_bounds__(C::WARPS * 32, 1)
     eval_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Args a) {
+    constexpr int WARPS = C::WARPS, R = C::R, BP = C::BP;
     constexpr int S = NS<KIND>::S;
     constexpr int PW = 128 / CW;       // positions per warp step
     constexpr int LPP = CW / 4;        // lanes per position
@@ -238,6 +258,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         __syncwarp();
     };
 
+    const unsigned long long policy = l2_policy(a.evict_last);
     const int pp = lane / LPP;  // position within a group
     const int vl = lane % LPP;  // 16-byte lane vector within the CW chunk
 
@@ -278,7 +299,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                 const int p = ig * PW + q;
                 if (ok[q])
                     tma_load_5d(dst + q * SLAB, &tmap, &bars[st_i], it.c * CW, __float_as_int(rc[p * REC + 38]),
-                                __float_as_int(rc[p * REC + 37]), __float_as_int(rc[p * REC + 36]) + ii, it.m);
+                                __float_as_int(rc[p * REC + 37]), __float_as_int(rc[p * REC + 36]) + ii, it.m,
+                                policy);
             }
         }
         if (++st_i == R) st_i = 0;
@@ -366,22 +388,40 @@ static EncodeTiled get_encode() {
     return fn;
 }
 
+template <class C>
 constexpr size_t smem_bytes() {
-    return (size_t)WARPS * R * STAGE + WARPS * (R + 2) * 8 + WARPS * 2 * BP * REC * 4 + WARPS * 2 * sizeof(ItemInfo);
+    return (size_t)C::WARPS * C::R * STAGE + C::WARPS * (C::R + 2) * 8 + C::WARPS * 2 * C::BP * REC * 4 +
+           C::WARPS * 2 * sizeof(ItemInfo);
 }
-static_assert(smem_bytes() <= 232448, "shared memory budget");
+static_assert(smem_bytes<CfgA>() <= 232448, "shared memory budget");
+static_assert(smem_bytes<CfgB>() <= 232448, "shared memory budget");
 
-template <int KIND, int CW>
-static int launch_t(const CUtensorMap &map, const Args &a, int grid, cudaStream_t st) {
-    constexpr size_t sm = smem_bytes();
-    cudaFuncSetAttribute(eval_tma_kernel<KIND, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    eval_tma_kernel<KIND, CW><<<grid, WARPS * 32, sm, st>>>(map, a);
+template <int KIND, int CW, class C>
+static int launch_t(const CUtensorMap &map, const Args &a, int sms, cudaStream_t st) {
+    constexpr size_t sm = smem_bytes<C>();
+    const long long warps_needed = (a.n_items + 1) / 2;
+    int grid = (int)min((long long)sms, (warps_needed + C::WARPS - 1) / C::WARPS);
+    if (grid < 1) grid = 1;
+    cudaFuncSetAttribute(eval_tma_kernel<KIND, CW, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    eval_tma_kernel<KIND, CW, C><<<grid, C::WARPS * 32, sm, st>>>(map, a);
     return check_launch("spo_eval (tma) launch");
 }
+
+template <int KIND, class C>
+static int launch_cw(int cw, const CUtensorMap &map, const Args &a, int sms, cudaStream_t st) {
+    switch (cw) {
+        case 32: return launch_t<KIND, 32, C>(map, a, sms, st);
+        case 64: return launch_t<KIND, 64, C>(map, a, sms, st);
+        default: return launch_t<KIND, 128, C>(map, a, sms, st);
+    }
+}
+
+
 
 }  // namespace tma
 
 long long eval_tma_workspace_bytes(long long n_pos) { return tma::WS_HEADER + n_pos * tma::REC * 4; }
+
 
 // Called by spo_eval for fp32 FAST requests with a workspace.  Returns -1
 // when the TMA path cannot be used (the caller then uses the generic kernel).
@@ -392,13 +432,13 @@ int eval_tma(int kind, const float *table, const TableGeom &geo, const GridArgs 
     if (!workspace || ws_bytes < eval_tma_workspace_bytes(n_pos) || !aligned16(workspace)) return -1;
     EncodeTiled encode = get_encode();
     if (!encode) return -1;
-    // chunk width: working set rows x CW x 4 B <= ~40 MB unless overridden
+    // chunk width: working set rows x CW x 4 B <= ~80 MB unless overridden
     const long long rows = (long long)geo.nxp * geo.nyp * geo.nzp;
     int cw = cw_request;
     if (cw == 0) {
         cw = 32;
-        if (rows * 128 * 4 <= (40LL << 20)) cw = 128;
-        else if (rows * 64 * 4 <= (40LL << 20)) cw = 64;
+        if (rows * 128 * 4 <= (80LL << 20)) cw = 128;
+        else if (rows * 64 * 4 <= (80LL << 20)) cw = 64;
     }
     while (cw > 32 && geo.nb % cw) cw >>= 1;
     if (cw < 32 || geo.nb % cw) return -1;
@@ -426,6 +466,9 @@ int eval_tma(int kind, const float *table, const TableGeom &geo, const GridArgs 
         if (rc) return rc;
     }
 
+    static const char *env_cfg = getenv("SPO_TMA_CFG");
+    const bool cfg_b = !(env_cfg && env_cfg[0] == '0');
+    const int BP = cfg_b ? CfgB::BP : CfgA::BP;
     Args a;
     a.recs = recs;
     a.ticket = reinterpret_cast<unsigned *>(ws);
@@ -438,24 +481,21 @@ int eval_tma(int kind, const float *table, const TableGeom &geo, const GridArgs 
     a.out_pos_stride = ops;
     a.out_stream_stride = oss;
     a.out_index = out_index;
+    static const char *env_hint = getenv("SPO_L2HINT");
+    a.evict_last = !(env_hint && env_hint[0] == '0');
     if (a.n_items >= (1LL << 32)) return -1;  // 32-bit ticket counter
 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const long long warps_needed = (a.n_items + 1) / 2;
-    int grid = (int)min((long long)sms, (warps_needed + WARPS - 1) / WARPS);
-    if (grid < 1) grid = 1;
-#define SPO_TMA_CASE(K)                                      \
-    switch (cw) {                                           \
-        case 32: return launch_t<K, 32>(map, a, grid, st);  \
-        case 64: return launch_t<K, 64>(map, a, grid, st);  \
-        default: return launch_t<K, 128>(map, a, grid, st); \
+    if (cfg_b) {
+        if (kind == SPO_KIND_V) return launch_cw<SPO_KIND_V, CfgB>(cw, map, a, sms, st);
+        if (kind == SPO_KIND_VGL) return launch_cw<SPO_KIND_VGL, CfgB>(cw, map, a, sms, st);
+        return launch_cw<SPO_KIND_VGH, CfgB>(cw, map, a, sms, st);
     }
-    if (kind == SPO_KIND_V) SPO_TMA_CASE(SPO_KIND_V)
-    if (kind == SPO_KIND_VGL) SPO_TMA_CASE(SPO_KIND_VGL)
-    SPO_TMA_CASE(SPO_KIND_VGH)
-#undef SPO_TMA_CASE
+    if (kind == SPO_KIND_V) return launch_cw<SPO_KIND_V, CfgA>(cw, map, a, sms, st);
+    if (kind == SPO_KIND_VGL) return launch_cw<SPO_KIND_VGL, CfgA>(cw, map, a, sms, st);
+    return launch_cw<SPO_KIND_VGH, CfgA>(cw, map, a, sms, st);
 }
 
 }  // namespace spo
