@@ -330,11 +330,18 @@ def run_b200(args):
     total_units = P * N * args.steps * world
     value = total_units / (elapsed_ms / 1e3)
 
+    from paper_1611_02665_b200 import _abi
+
+    pipelined = args.mode == "fast" and _abi.load().spo_eval_workspace_bytes(
+        KernelKind(kind).code, 0, 0, chunk) > 0
+    kernels_per_call = 2 if pipelined else 1  # prologue_records_kernel + eval_tma_kernel
+    kernel_name = (f"spo::tma::eval_tma_kernel<{kind.upper()}> (+ prologue_records_kernel, timed together)"
+                   if pipelined else f"spo::eval_kernel<{kind.upper()},float,{args.mode}>")
     peak, peak_src = measured_peak()
     achieved = bpp * chunk / (avg_launch_ms * 1e-3) / 1e9  # GB/s per launch
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(args, cfg, kind, chunk),
-                "peak_source": peak_src, "kernel": f"spo::eval_kernel<{kind.upper()},float,{args.mode}>",
+                "peak_source": peak_src, "kernel": kernel_name,
                 "algorithmic_bytes_per_position": bpp, "positions_per_launch": chunk,
                 "avg_launch_ms": avg_launch_ms}
 
@@ -352,7 +359,7 @@ def run_b200(args):
                    "l2": f"inputs larger than L2 (table {table.nbytes / 1e9:.2f} GB >> 126 MB); no flush",
                    "parallelism": f"walker-sharded x{world}, table replicated"},
         "roofline": roofline,
-        "gpu_launches": len(bounds) * args.steps,
+        "gpu_launches": len(bounds) * args.steps * kernels_per_call,
         "clocks": clocks.summary(wall0, wall1),
     }
 

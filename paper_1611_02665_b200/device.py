@@ -14,6 +14,7 @@ slices, so a tile-major sweep keeps one slice L2-resident.
 from __future__ import annotations
 
 import ctypes
+import warnings
 import weakref
 
 import numpy as np
@@ -152,7 +153,9 @@ class DeviceTable:
         g = table.grid
         grid = g if isinstance(g, GridSpec) else GridSpec(g.nx, g.ny, g.nz, g.dx, g.dy, g.dz)
         dt = cls.empty(grid, n, data.dtype, ts, device)
-        src = torch.from_numpy(data).to(dt.device)
+        with warnings.catch_warnings():  # read-only host tables are only read
+            warnings.simplefilter("ignore", UserWarning)
+            src = torch.from_numpy(data).to(dt.device)
         _abi.check(_abi.load().spo_pack_table(dt.dtype_code, src.data_ptr(), src_npad, n,
                                               _abi.i32x3(grid.counts), dt.tile_size, dt.nb,
                                               dt.n_tiles, dt.data.data_ptr(), _stream_ptr(dt.device)))

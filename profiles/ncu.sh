@@ -14,6 +14,6 @@ $CMD > gpurun_out/bench_${TAG}.log 2>&1 || { echo "plain bench failed"; exit 1; 
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launches_${TAG}.log 2>&1
 $SMALL > gpurun_out/small_${TAG}.log 2>&1 || { echo "small bench failed"; exit 1; }
-ncu --set full --clock-control none --import-source on -k regex:eval_kernel -s 1 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:eval_tma_kernel -s 1 -c 1 \
     -o gpurun_out/prof_${TAG} -f $SMALL > gpurun_out/ncu_full_${TAG}.log 2>&1
 echo "done"
