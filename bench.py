@@ -51,9 +51,9 @@ def parse():
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--kind", default=None, help="override the config kernel (v/vgl/vgh)")
-    ap.add_argument("--chunk", type=int, default=1 << 16)
+    ap.add_argument("--chunk", type=int, default=1 << 18)
     ap.add_argument("--mode", default="fast", choices=("fast", "strict"))
-    ap.add_argument("--tile", type=int, default=0, help="AoSoA tile size (0 = untiled)")
+    ap.add_argument("--tile", type=int, default=-1, help="AoSoA tile size (-1 = auto, 0 = untiled)")
     ap.add_argument("--walkers", type=int, default=0, help="override walkers per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu", action="store_true")
@@ -257,7 +257,8 @@ def run_b200(args):
     P = pos_np.shape[0]
     N = cfg.n_splines
     S = KernelKind(kind).output_streams_soa
-    table = DeviceTable.random(cfg.grid, N, seed=0, tile_size=args.tile or None, device=dev)
+    tile = "auto" if args.tile < 0 else (args.tile or None)
+    table = DeviceTable.random(cfg.grid, N, seed=0, tile_size=tile, device=dev)
     pos = torch.from_numpy(pos_np).to(dev)
     chunk = min(args.chunk, P)
     out = torch.empty((chunk, S, table.lanes), dtype=torch.float32, device=dev)

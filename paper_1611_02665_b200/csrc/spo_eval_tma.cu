@@ -196,18 +196,29 @@ template <int WARPS_, int R_, int BP_>
 struct TCfg {
     static constexpr int WARPS = WARPS_, R = R_, BP = BP_;
 };
-using CfgA = TCfg<8, 3, 12>;   // 8 warps, 2 slabs in flight per warp
-using CfgB = TCfg<12, 2, 8>;   // 12 warps, 1 slab in flight per warp
+using CfgB = TCfg<12, 2, 8>;   // 12 warps, one slab in flight per warp while it computes one
 
 struct ItemInfo {
     long long b0;
     int nb, m, c, G, valid, pad;
 };
 
+// Issue descriptor of one group (lane 0's registers): per position the
+// TMA coordinates and whether it is valid; the chunk/tile of the item.
+template <int PW>
+struct GroupDesc {
+    int x[PW], y[PW], z[PW];  // i0, j0, k0 (z = k0 is the fastest table dim after lanes)
+    unsigned bytes;           // valid positions x slab bytes
+    int c0, m;
+    bool any;
+};
+
 template <int KIND, int CW, class C>
 __global__ void __launch_bounds__(C::WARPS * 32, 1)
     eval_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Args a) {
-    constexpr int WARPS = C::WARPS, R = C::R, BP = C::BP;
+    constexpr int WARPS = C::WARPS, BP = C::BP;
+    static_assert(C::R == 2, "the issue path runs exactly one slab ahead");
+    constexpr int R = 2;
     constexpr int S = NS<KIND>::S;
     constexpr int PW = 128 / CW;       // positions per warp step
     constexpr int LPP = CW / 4;        // lanes per position
@@ -258,67 +269,57 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
         __syncwarp();
     };
 
+    // lane 0: descriptor of group g of the item in `slot` (records must have landed)
+    auto prepare = [&](GroupDesc<PW> &d, int slot, int g) {
+        const ItemInfo it = info[slot];
+        const float *rc = recs + slot * BP * REC;
+        d.bytes = 0;
+        d.c0 = it.c * CW;
+        d.m = it.m;
+#pragma unroll
+        for (int q = 0; q < PW; ++q) {
+            const int p = g * PW + q;
+            const int4 cell = *reinterpret_cast<const int4 *>(rc + min(p, it.nb - 1) * REC + 36);
+            const bool ok = p < it.nb && cell.x >= 0;
+            d.x[q] = ok ? cell.x : -1;
+            d.y[q] = cell.y;
+            d.z[q] = cell.z;
+            d.bytes += ok ? SLAB : 0;
+        }
+        d.any = true;
+    };
+    // lane 0: issue slab ii of the described group into stage st
+    auto issue = [&](const GroupDesc<PW> &d, int ii, int st, unsigned long long policy) {
+        unsigned char *dst = ring + st * STAGE;
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&bars[st], d.bytes);
+#pragma unroll
+        for (int q = 0; q < PW; ++q)
+            if (d.x[q] >= 0) tma_load_5d(dst + q * SLAB, &tmap, &bars[st], d.c0, d.z[q], d.y[q], d.x[q] + ii, d.m, policy);
+    };
+
     const unsigned long long policy = l2_policy(a.evict_last);
     const int pp = lane / LPP;  // position within a group
     const int vl = lane % LPP;  // 16-byte lane vector within the CW chunk
 
-    int st_i = 0, st_c = 0;  // issue / consume stage indices (same sequence, R-1 apart)
-    unsigned ph_c = 0;       // consume phase parity of stage st_c
-    unsigned rph0 = 0, rph1 = 0;
+    unsigned ph0 = 0, ph1 = 0;    // stage barrier parities
+    unsigned rph0 = 0, rph1 = 0;  // record barrier parities
+    GroupDesc<PW> d;
+    d.any = false;
 
     fill(0);
     fill(1);
-
-    // issue cursor
-    int islot = 0, ig = 0, ii = 0;
-    bool iactive = info[0].valid, iready = false;
-    auto issue_next = [&]() {
-        if (!iactive) return;
-        if (!iready) {  // records of this slot must have landed (cells + weights)
-            mbar_wait(&rbar[islot], islot ? rph1 : rph0);
-            if (islot) rph1 ^= 1; else rph0 ^= 1;
-            iready = true;
-        }
-        __syncwarp();  // every lane is done reading this stage (WAR vs TMA)
-        if (lane == 0) {
-            const ItemInfo it = info[islot];
-            const float *rc = recs + islot * BP * REC;
-            unsigned char *dst = ring + st_i * STAGE;
-            bool ok[PW];
-            unsigned bytes = 0;
-#pragma unroll
-            for (int q = 0; q < PW; ++q) {
-                const int p = ig * PW + q;
-                ok[q] = p < it.nb && __float_as_int(rc[p * REC + 36]) >= 0;
-                bytes += ok[q] ? SLAB : 0;
-            }
-            fence_proxy_async();
-            mbar_arrive_expect_tx(&bars[st_i], bytes);
-#pragma unroll
-            for (int q = 0; q < PW; ++q) {
-                const int p = ig * PW + q;
-                if (ok[q])
-                    tma_load_5d(dst + q * SLAB, &tmap, &bars[st_i], it.c * CW, __float_as_int(rc[p * REC + 38]),
-                                __float_as_int(rc[p * REC + 37]), __float_as_int(rc[p * REC + 36]) + ii, it.m,
-                                policy);
-            }
-        }
-        if (++st_i == R) st_i = 0;
-        if (++ii == 4) {
-            ii = 0;
-            if (++ig == info[islot].G) {
-                ig = 0;
-                islot ^= 1;
-                iready = false;
-                iactive = info[islot].valid;
-            }
-        }
-    };
-
-    for (int t = 0; t < R - 1; ++t) issue_next();
+    if (!info[0].valid) return;
+    mbar_wait(&rbar[0], rph0);
+    rph0 ^= 1;
+    if (lane == 0) {
+        prepare(d, 0, 0);
+        issue(d, 0, 0, policy);
+    }
+    int st = 0;  // stage of the step being consumed; the next step goes to st ^ 1
 
     int cslot = 0;
-    while (info[cslot].valid) {
+    while (true) {
         const ItemInfo it = info[cslot];
         const float *rc = recs + cslot * BP * REC;
         for (int g = 0; g < it.G; ++g) {
@@ -342,14 +343,41 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
                 for (int e = 0; e < 4; ++e) acc[s][e] = 0.0f;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                issue_next();
-                mbar_wait(&bars[st_c], ph_c);
-                const float *slab = reinterpret_cast<const float *>(ring + st_c * STAGE + pp * SLAB) + vl * 4;
-                slab_fma<KIND, CW>(slab, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
-                if (++st_c == R) {
-                    st_c = 0;
-                    ph_c ^= 1;
+                // ---- issue the next step into the other stage (its previous
+                // contents were consumed in the step before this one)
+                __syncwarp();
+                if (i < 3) {
+                    if (lane == 0) issue(d, i + 1, st ^ 1, policy);
+                } else if (g + 1 < it.G) {
+                    if (lane == 0) {
+                        prepare(d, cslot, g + 1);
+                        issue(d, 0, st ^ 1, policy);
+                    }
+                } else if (info[cslot ^ 1].valid) {
+                    // first group of the next item: its records must have landed
+                    if (cslot) {
+                        mbar_wait(&rbar[0], rph0);
+                        rph0 ^= 1;
+                    } else {
+                        mbar_wait(&rbar[1], rph1);
+                        rph1 ^= 1;
+                    }
+                    if (lane == 0) {
+                        prepare(d, cslot ^ 1, 0);
+                        issue(d, 0, st ^ 1, policy);
+                    }
                 }
+                // ---- consume this step
+                if (st) {
+                    mbar_wait(&bars[1], ph1);
+                    ph1 ^= 1;
+                } else {
+                    mbar_wait(&bars[0], ph0);
+                    ph0 ^= 1;
+                }
+                const float *slab = reinterpret_cast<const float *>(ring + st * STAGE + pp * SLAB) + vl * 4;
+                slab_fma<KIND, CW>(slab, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
+                st ^= 1;
             }
             if (p < it.nb) {
                 const long long gp = it.b0 + p;
@@ -364,7 +392,9 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
             }
         }
         __syncwarp();
-        fill(cslot);  // the issue cursor has left this slot: refill it with the next ticket
+        const bool more = info[cslot ^ 1].valid;
+        fill(cslot);  // the issue path has left this slot: refill it with the next ticket
+        if (!more) break;
         cslot ^= 1;
     }
 }
@@ -393,7 +423,6 @@ constexpr size_t smem_bytes() {
     return (size_t)C::WARPS * C::R * STAGE + C::WARPS * (C::R + 2) * 8 + C::WARPS * 2 * C::BP * REC * 4 +
            C::WARPS * 2 * sizeof(ItemInfo);
 }
-static_assert(smem_bytes<CfgA>() <= 232448, "shared memory budget");
 static_assert(smem_bytes<CfgB>() <= 232448, "shared memory budget");
 
 template <int KIND, int CW, class C>
@@ -466,9 +495,7 @@ int eval_tma(int kind, const float *table, const TableGeom &geo, const GridArgs 
         if (rc) return rc;
     }
 
-    static const char *env_cfg = getenv("SPO_TMA_CFG");
-    const bool cfg_b = !(env_cfg && env_cfg[0] == '0');
-    const int BP = cfg_b ? CfgB::BP : CfgA::BP;
+    const int BP = CfgB::BP;
     Args a;
     a.recs = recs;
     a.ticket = reinterpret_cast<unsigned *>(ws);
@@ -488,14 +515,9 @@ int eval_tma(int kind, const float *table, const TableGeom &geo, const GridArgs 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cfg_b) {
-        if (kind == SPO_KIND_V) return launch_cw<SPO_KIND_V, CfgB>(cw, map, a, sms, st);
-        if (kind == SPO_KIND_VGL) return launch_cw<SPO_KIND_VGL, CfgB>(cw, map, a, sms, st);
-        return launch_cw<SPO_KIND_VGH, CfgB>(cw, map, a, sms, st);
-    }
-    if (kind == SPO_KIND_V) return launch_cw<SPO_KIND_V, CfgA>(cw, map, a, sms, st);
-    if (kind == SPO_KIND_VGL) return launch_cw<SPO_KIND_VGL, CfgA>(cw, map, a, sms, st);
-    return launch_cw<SPO_KIND_VGH, CfgA>(cw, map, a, sms, st);
+    if (kind == SPO_KIND_V) return launch_cw<SPO_KIND_V, CfgB>(cw, map, a, sms, st);
+    if (kind == SPO_KIND_VGL) return launch_cw<SPO_KIND_VGL, CfgB>(cw, map, a, sms, st);
+    return launch_cw<SPO_KIND_VGH, CfgB>(cw, map, a, sms, st);
 }
 
 }  // namespace spo

@@ -40,6 +40,29 @@ def _round_up(n: int, q: int) -> int:
     return ((n + q - 1) // q) * q
 
 
+# L2 working-set target for one AoSoA tile slice (of 126 MB L2; the output
+# stream and the next unit share the rest).
+TILE_SLICE_BYTES = 80 << 20
+
+
+def auto_tile_size(grid: GridSpec, n_splines: int, dtype=np.float32):
+    """AoSoA tile width (splines) so that one tile slice -- (n+3)^3 rows x tile
+    lanes -- fits the L2 working-set target: 128, 64 or 32 lanes (the TMA
+    kernel's chunk widths); untiled when N fits in one such tile.  Tiles are
+    multiples of the 128-byte lane quantum, so spline n keeps output lane n."""
+    rows = int(np.prod(grid.padded_counts))
+    item = np.dtype(dtype).itemsize
+    q = lane_quantum(dtype)
+    tile = q
+    for cand in (128, 64, 32):
+        if cand % q == 0 and rows * cand * item <= TILE_SLICE_BYTES:
+            tile = cand
+            break
+    if n_splines <= tile:
+        return None
+    return tile
+
+
 def _resolve_device(device):
     torch = _torch()
     if not torch.cuda.is_available():
@@ -107,6 +130,8 @@ class DeviceTable:
 
     @staticmethod
     def _shape(grid, n_splines, dtype, tile_size):
+        if tile_size == "auto":
+            tile_size = auto_tile_size(grid, n_splines, dtype)
         tile_size = int(tile_size or n_splines)
         if tile_size < 1:
             raise ConfigError(f"tile_size={tile_size} must be >= 1")
@@ -116,7 +141,7 @@ class DeviceTable:
 
     # ----------------------------------------------------- construction --
     @classmethod
-    def empty(cls, grid, n_splines, dtype=np.float32, tile_size=None, device=None):
+    def empty(cls, grid, n_splines, dtype=np.float32, tile_size="auto", device=None):
         torch = _torch()
         device = _resolve_device(device)
         tile_size, shape = cls._shape(grid, n_splines, dtype, tile_size)
@@ -124,7 +149,7 @@ class DeviceTable:
         return cls(grid, n_splines, dtype, tile_size, torch.empty(shape, dtype=tdt, device=device))
 
     @classmethod
-    def from_host(cls, table, tile_size=None, device=None) -> "DeviceTable":
+    def from_host(cls, table, tile_size="auto", device=None) -> "DeviceTable":
         """Upload a reference-style host table (CoeffTableSoA / TiledCoeffTable /
         CoeffTableAoS, from this package or from bspb itself)."""
         torch = _torch()
@@ -134,7 +159,7 @@ class DeviceTable:
             data = np.concatenate([np.asarray(t.data)[..., : t.n_splines] for t in tiles], axis=-1)
             n = data.shape[-1]
             src_npad = n
-            ts = tile_size or table.tile_size
+            ts = table.tile_size if tile_size in (None, "auto") else tile_size
         elif layout == "aos" or isinstance(table, CoeffTableAoS):
             data = np.moveaxis(np.asarray(table.data), 0, -1)
             n = table.n_splines
@@ -163,7 +188,7 @@ class DeviceTable:
         return dt
 
     @classmethod
-    def random(cls, grid, n_splines, seed=0, tile_size=None, device=None) -> "DeviceTable":
+    def random(cls, grid, n_splines, seed=0, tile_size="auto", device=None) -> "DeviceTable":
         """FillSpec.random(seed) generated on the device, bit-identical to
         build_table(grid, N, FillSpec.random(seed)) (coeffs.py:80-94, 165-185)."""
         torch = _torch()
@@ -176,7 +201,7 @@ class DeviceTable:
         return dt
 
     @classmethod
-    def normal_f64(cls, grid, n_splines, seed=0, tile_size=None, device=None) -> "DeviceTable":
+    def normal_f64(cls, grid, n_splines, seed=0, tile_size="auto", device=None) -> "DeviceTable":
         """Builder-defined fp64 N(0,1) table (BASELINE config 5; spo_b200.h)."""
         torch = _torch()
         dt = cls.empty(grid, n_splines, np.float64, tile_size, device)
