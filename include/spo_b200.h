@@ -23,6 +23,8 @@
  *   spo_fill_uniform  replaces coeffs.py:80-94 + 165-185 (FillSpec.random +
  *                   build_table): numpy Philox4x64 streams, bit-identical,
  *                   generated straight into the device layout.
+ *   spo_fill_positions  replaces driver.py:174-193 (generate_positions): the
+ *                   walker Philox position streams, bit-identical, on device.
  *   spo_fill_normal_f64  builder-defined N(0,1) fill for the fp64 config
  *                   (no reference equivalent).
  *   spo_last_error  error text for the last failing call on this thread; the
@@ -151,6 +153,16 @@ int spo_fill_uniform(const uint64_t *keys, int32_t n_splines, const int32_t *n3,
 int spo_fill_normal_f64(const uint64_t *keys, int32_t n_splines, const int32_t *n3,
                         int32_t tile_size, int32_t nb, int32_t n_tiles, double *dst,
                         void *stream);
+
+/*
+ * Walker position streams generated on the device, bit-identical to the
+ * reference's driver.py:174-179 _position_stream(seed, walker, iteration,
+ * kernel_id, ns, grid) for walkers walker0 .. walker0+n_walkers-1:
+ * out [n_walkers*ns][3] float64 (device), lengths3 = GridSpec.lengths (host).
+ */
+int spo_fill_positions(uint64_t seed, int64_t walker0, int64_t n_walkers, uint64_t iteration,
+                       uint64_t kernel_id, int64_t ns, const double *lengths3, double *out,
+                       void *stream);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,7 @@ ABI_VERSION = 2
 EXPORTS = ("spo_abi_version", "spo_last_error", "spo_eval", "spo_eval_workspace_bytes", "spo_prologue",
            "spo_basis_weights",
            "spo_pack_table",
-           "spo_fill_uniform", "spo_fill_normal_f64")
+           "spo_fill_uniform", "spo_fill_normal_f64", "spo_fill_positions")
 
 _lock = threading.Lock()
 _lib = None
@@ -66,6 +66,9 @@ def load(build_if_missing: bool = True):
         L.spo_fill_uniform.argtypes = [vp, i32, P(i32), i32, i32, i32, vp, vp]
         L.spo_fill_normal_f64.restype = ip
         L.spo_fill_normal_f64.argtypes = [vp, i32, P(i32), i32, i32, i32, vp, vp]
+        u64 = ctypes.c_uint64
+        L.spo_fill_positions.restype = ip
+        L.spo_fill_positions.argtypes = [u64, i64, i64, u64, u64, i64, P(dbl), vp, vp]
         if L.spo_abi_version() != ABI_VERSION:
             raise RuntimeError("libspo_b200.so ABI version mismatch; rebuild")
         _lib = L

@@ -124,6 +124,30 @@ __global__ void fill_normal_kernel(const unsigned long long *__restrict__ keys, 
     }
 }
 
+// driver.py:174-179 _position_stream: Philox(counter=[0, walker, iteration,
+// kernel_id], key=[seed, 0]).random((ns, 3)) * lengths.  Element e = 3 s + axis
+// is 64-bit word e of the stream: block e/4 uses counter[0] = e/4 + 1 (numpy
+// increments before generating), lane e % 4; next_double = (w >> 11) * 2^-53.
+__global__ void positions_kernel(unsigned long long seed, long long walker0, long long n_walkers,
+                                 unsigned long long iteration, unsigned long long kernel_id, long long ns,
+                                 double lx, double ly, double lz, double *__restrict__ out) {
+    const long long total = n_walkers * ns * 3;
+    for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
+         g += (long long)gridDim.x * blockDim.x) {
+        const long long w = g / (ns * 3);
+        const unsigned long long e = (unsigned long long)(g - w * ns * 3);
+        U4 c;
+        c.v[0] = (e >> 2) + 1ULL;
+        c.v[1] = (unsigned long long)(walker0 + w);
+        c.v[2] = iteration;
+        c.v[3] = kernel_id;
+        const U4 o = philox4x64_10(c, seed, 0ULL);
+        const double u = (double)(o.v[e & 3] >> 11) * (1.0 / 9007199254740992.0);
+        const int axis = (int)(e % 3);
+        out[g] = __dmul_rn(u, axis == 0 ? lx : (axis == 1 ? ly : lz));
+    }
+}
+
 static int make_pack_geom(int dtype, int32_t n_splines, const int32_t *n3, int32_t tile_size,
                           int32_t nb, int32_t n_tiles, PackGeom *g) {
     TableGeom t;
@@ -196,4 +220,16 @@ extern "C" int spo_fill_normal_f64(const uint64_t *keys, int32_t n_splines, cons
     fill_normal_kernel<<<grid_for(g.total), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
         reinterpret_cast<const unsigned long long *>(keys), g, dst);
     return check_launch("spo_fill_normal_f64");
+}
+
+extern "C" int spo_fill_positions(uint64_t seed, int64_t walker0, int64_t n_walkers, uint64_t iteration,
+                                  uint64_t kernel_id, int64_t ns, const double *lengths3, double *out,
+                                  void *stream) {
+    if (n_walkers < 0 || ns < 0) return fail(SPO_ERR_CONTRACT, "negative walker or sample count");
+    if (n_walkers == 0 || ns == 0) return ok();
+    if (!out || !lengths3) return fail(SPO_ERR_CONTRACT, "NULL pointer");
+    const long long total = n_walkers * ns * 3;
+    positions_kernel<<<grid_for(total), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        seed, walker0, n_walkers, iteration, kernel_id, ns, lengths3[0], lengths3[1], lengths3[2], out);
+    return check_launch("spo_fill_positions");
 }

@@ -125,3 +125,23 @@ def bytes_per_position(kind: str, n_splines: int, itemsize: int = 4, quantum: in
     npad = ((n_splines + quantum - 1) // quantum) * quantum
     s = {"v": 1, "vgl": 5, "vgh": 10}[kind]
     return 64 * npad * itemsize + s * npad * itemsize
+
+
+def device_walker_positions(seed, walker0, n_walkers, iteration, kernel: str, ns, grid: GridSpec,
+                            device=None, out=None):
+    """walker_positions generated on the device (spo_fill_positions),
+    bit-identical to the numpy streams: (n_walkers * ns, 3) float64 CUDA tensor."""
+    import ctypes
+
+    import torch
+
+    from . import _abi
+    from .device import _resolve_device, _stream_ptr
+
+    device = _resolve_device(device)
+    if out is None:
+        out = torch.empty((n_walkers * ns, 3), dtype=torch.float64, device=device)
+    _abi.check(_abi.load().spo_fill_positions(
+        ctypes.c_uint64(int(seed) % (1 << 64)), int(walker0), int(n_walkers), int(iteration),
+        KERNEL_STREAM_ID[kernel], int(ns), _abi.f64x3(grid.lengths), out.data_ptr(), _stream_ptr(device)))
+    return out
