@@ -116,7 +116,7 @@ class ClockSampler:
     def summary(self, t0=None, t1=None):
         """Median SM clock and active throttle reasons over samples taken in
         [t0, t1] (the timed region), falling back to all samples under load."""
-        sm, mx, reasons = [], 0.0, set()
+        sm, pw, mx, reasons = [], [], 0.0, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         lines = [ln for ts, ln in self.lines if t0 is None or t0 - 0.25 <= ts <= t1 + 0.25]
         window = "timed region"
@@ -129,6 +129,7 @@ class ClockSampler:
                 continue
             try:
                 sm.append(float(f[1]))
+                pw.append(float(f[3]))
                 mx = max(mx, float(f[2]))
             except ValueError:
                 continue
@@ -138,7 +139,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm), "window": window}
+                "power_w": statistics.median(pw), "samples": len(sm), "window": window}
 
 
 def workload(args, rank):

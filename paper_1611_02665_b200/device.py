@@ -212,7 +212,7 @@ class DeviceTable:
         torch.cuda.current_stream(dt.device).synchronize()
         return dt
 
-    def slice_orbitals(self, lo: int, hi: int, tile_size=None) -> "DeviceTable":
+    def slice_orbitals(self, lo: int, hi: int, tile_size="auto") -> "DeviceTable":
         """A new device table holding splines [lo, hi) (orbital sharding)."""
         ref = self.reference_soa(device_result=True)
         torch = _torch()

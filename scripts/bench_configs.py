@@ -1,0 +1,107 @@
+#!/usr/bin/env python
+"""Throughput of every BASELINE config on one B200 (the BASELINE.md report
+template): orbital-evals/s, algorithmic GB/s and the fraction of the measured
+HBM bandwidth, per kernel kind.  Inputs are generated on the device with the
+reference's streams (table: FillSpec.random(0); positions: walker streams,
+seed 1).  Timing: CUDA events around each config's launches after a warm-up
+pass, best of `--reps` repetitions.
+
+    python scripts/bench_configs.py [--configs 1,2,3,4,5] [--reps 3] [--md out.md]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def timed(fn, reps):
+    import torch
+
+    fn()
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) * 1e-3)
+    return best
+
+
+def main():
+    import torch
+
+    from paper_1611_02665_b200 import DeviceTable, evaluate
+    from paper_1611_02665_b200.multi import OrbitalPartition
+    from paper_1611_02665_b200.workloads import CONFIGS, bytes_per_position, config_positions
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,2,3,4,5")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--md", default=None)
+    args = ap.parse_args()
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        peak = float(json.load(f)["hbm_gbs"])
+    rows = []
+    chunk = 1 << 17
+    for idx in [int(c) for c in args.configs.split(",")]:
+        cfg = CONFIGS[idx]
+        if cfg.dtype == "f64":
+            full = DeviceTable.normal_f64(cfg.grid, cfg.n_splines, seed=0)
+            part = OrbitalPartition.make(cfg.n_splines, 8, quantum=16)
+            shard = full.slice_orbitals(*part.local(0))
+            del full
+            tables = {"per-GPU shard (N/8 = 512)": shard}
+            pos = config_positions(cfg)  # all 2,097,152 positions, 12:1:1
+            item, q = 8, 16
+        else:
+            tables = {"full table": DeviceTable.random(cfg.grid, cfg.n_splines, seed=0)}
+            pos = config_positions(cfg)
+            item, q = 4, 32
+        for tname, dt in tables.items():
+            for kind, p in pos.items():
+                if idx == 1:
+                    p = p[:512]
+                P = p.shape[0]
+                dp = torch.from_numpy(np.ascontiguousarray(p)).cuda()
+                S = {"v": 1, "vgl": 5, "vgh": 10}[kind]
+                c = min(chunk, P)
+                out = torch.empty((c, S, dt.lanes), dtype=dt.data.dtype, device="cuda")
+
+                def run():
+                    for lo in range(0, P, c):
+                        evaluate(dt, kind, dp[lo: lo + c], out[: min(c, P - lo)], check=False)
+
+                t = timed(run, args.reps)
+                bpp = bytes_per_position(kind, dt.n_splines, item, q)
+                gbs = bpp * P / t / 1e9
+                rows.append({"config": idx, "table": tname, "kind": kind, "positions": P,
+                             "n_splines": dt.n_splines, "dtype": cfg.dtype, "seconds": t,
+                             "orbital_evals_per_s": P * dt.n_splines / t, "algorithmic_gbs": gbs,
+                             "fraction_of_hbm": gbs / peak})
+                print(json.dumps(rows[-1]), flush=True)
+        del tables
+        torch.cuda.empty_cache()
+    if args.md:
+        with open(args.md, "w") as f:
+            f.write("| cfg | table | kernel | positions | N | dtype | time (ms) | orbital-evals/s | "
+                    "algorithmic GB/s | fraction of %.1f GB/s |\n" % peak)
+            f.write("|---|---|---|---|---|---|---|---|---|---|\n")
+            for r in rows:
+                f.write(f"| {r['config']} | {r['table']} | {r['kind'].upper()} | {r['positions']:,} | "
+                        f"{r['n_splines']} | {r['dtype']} | {r['seconds'] * 1e3:.3f} | "
+                        f"{r['orbital_evals_per_s']:.3e} | {r['algorithmic_gbs']:,.0f} | "
+                        f"{r['fraction_of_hbm']:.3f} |\n")
+
+
+if __name__ == "__main__":
+    main()
