@@ -110,6 +110,66 @@ struct NS {
     static constexpr int S = KIND == SPO_KIND_V ? 1 : (KIND == SPO_KIND_VGL ? 5 : 10);
 };
 
+// Packed fp32x2 FMA (SASS FFMA2, sm_100): two independent round-to-nearest
+// fp32 FMAs per instruction with a broadcast scalar multiplier -- bitwise the
+// same as two __fmaf_rn, at half the issue slots.
+__device__ __forceinline__ float2 fma2(float w, float2 c, float2 acc) {
+    return __ffma2_rn(make_float2(w, w), c, acc);
+}
+__device__ __forceinline__ float2 mul2(float w, float2 c) { return __fmul2_rn(make_float2(w, w), c); }
+
+// slab_fma with the 4 orbitals of a lane handled as two fp32x2 pairs.
+template <int KIND, int CW>
+__device__ __forceinline__ void slab_fma2(const float *__restrict__ slab, const float (&wy)[12],
+                                          const float (&wz)[12], float ax, float dax, float d2ax,
+                                          float2 (&acc)[NS<KIND>::S][2]) {
+    float2 t00[2], t10[2], t01[2], t20[2], t11[2], t02[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) t00[h] = t10[h] = t01[h] = t20[h] = t11[h] = t02[h] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float4 c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const float4 *>(slab + (j * 4 + k) * CW);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float2 c0 = h ? make_float2(c[0].z, c[0].w) : make_float2(c[0].x, c[0].y);
+            const float2 c1 = h ? make_float2(c[1].z, c[1].w) : make_float2(c[1].x, c[1].y);
+            const float2 c2 = h ? make_float2(c[2].z, c[2].w) : make_float2(c[2].x, c[2].y);
+            const float2 c3 = h ? make_float2(c[3].z, c[3].w) : make_float2(c[3].x, c[3].y);
+            const float2 s0 = fma2(wz[3], c3, fma2(wz[2], c2, fma2(wz[1], c1, mul2(wz[0], c0))));
+            t00[h] = fma2(wy[j], s0, t00[h]);
+            if (KIND != SPO_KIND_V) {
+                const float2 s1 = fma2(wz[7], c3, fma2(wz[6], c2, fma2(wz[5], c1, mul2(wz[4], c0))));
+                const float2 s2 = fma2(wz[11], c3, fma2(wz[10], c2, fma2(wz[9], c1, mul2(wz[8], c0))));
+                t10[h] = fma2(wy[4 + j], s0, t10[h]);
+                t01[h] = fma2(wy[j], s1, t01[h]);
+                t20[h] = fma2(wy[8 + j], s0, t20[h]);
+                t02[h] = fma2(wy[j], s2, t02[h]);
+                if (KIND == SPO_KIND_VGH) t11[h] = fma2(wy[4 + j], s1, t11[h]);
+            }
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        acc[0][h] = fma2(ax, t00[h], acc[0][h]);
+        if (KIND != SPO_KIND_V) {
+            acc[1][h] = fma2(dax, t00[h], acc[1][h]);
+            acc[2][h] = fma2(ax, t10[h], acc[2][h]);
+            acc[3][h] = fma2(ax, t01[h], acc[3][h]);
+        }
+        if (KIND == SPO_KIND_VGL) acc[4][h] = fma2(d2ax, t00[h], fma2(ax, t20[h], fma2(ax, t02[h], acc[4][h])));
+        if (KIND == SPO_KIND_VGH) {
+            acc[4][h] = fma2(d2ax, t00[h], acc[4][h]);
+            acc[5][h] = fma2(dax, t10[h], acc[5][h]);
+            acc[6][h] = fma2(dax, t01[h], acc[6][h]);
+            acc[7][h] = fma2(ax, t20[h], acc[7][h]);
+            acc[8][h] = fma2(ax, t11[h], acc[8][h]);
+            acc[9][h] = fma2(ax, t02[h], acc[9][h]);
+        }
+    }
+}
+
 // One i-slab of the separable contraction for one 16-byte lane vector.
 // slab: [j][k][CW] floats of this lane's position; wy/wz: 12 weights each;
 // ax/dax/d2ax: the x weights of this i.
@@ -336,11 +396,9 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
                 wz[e] = z4.x, wz[e + 1] = z4.y, wz[e + 2] = z4.z, wz[e + 3] = z4.w;
             }
             const bool finite = __float_as_int(w[36]) >= 0;
-            float acc[S][4];
+            float2 acc[S][2];
 #pragma unroll
-            for (int s = 0; s < S; ++s)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) acc[s][e] = 0.0f;
+            for (int s = 0; s < S; ++s) acc[s][0] = acc[s][1] = make_float2(0.0f, 0.0f);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 // ---- issue the next step into the other stage (its previous
@@ -376,7 +434,7 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
                     ph0 ^= 1;
                 }
                 const float *slab = reinterpret_cast<const float *>(ring + st * STAGE + pp * SLAB) + vl * 4;
-                slab_fma<KIND, CW>(slab, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
+                slab_fma2<KIND, CW>(slab, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
                 st ^= 1;
             }
             if (p < it.nb) {
@@ -385,7 +443,7 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
                 float *o = a.out + op * a.out_pos_stride + (long long)it.m * a.nb + it.c * CW + vl * 4;
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
-                    const float4 v = finite ? make_float4(acc[s][0], acc[s][1], acc[s][2], acc[s][3])
+                    const float4 v = finite ? make_float4(acc[s][0].x, acc[s][0].y, acc[s][1].x, acc[s][1].y)
                                             : make_float4(NAN, NAN, NAN, NAN);
                     __stcs(reinterpret_cast<float4 *>(o + s * a.out_stream_stride), v);
                 }
@@ -461,13 +519,14 @@ int eval_tma(int kind, const float *table, const TableGeom &geo, const GridArgs 
     if (!workspace || ws_bytes < eval_tma_workspace_bytes(n_pos) || !aligned16(workspace)) return -1;
     EncodeTiled encode = get_encode();
     if (!encode) return -1;
-    // chunk width: working set rows x CW x 4 B <= ~80 MB unless overridden
+    // chunk width: working set rows x CW x 4 B <= ~40 MB unless overridden (one
+    // die's share of L2, with room for the next unit and the output stream)
     const long long rows = (long long)geo.nxp * geo.nyp * geo.nzp;
     int cw = cw_request;
     if (cw == 0) {
         cw = 32;
-        if (rows * 128 * 4 <= (80LL << 20)) cw = 128;
-        else if (rows * 64 * 4 <= (80LL << 20)) cw = 64;
+        if (rows * 128 * 4 <= (40LL << 20)) cw = 128;
+        else if (rows * 64 * 4 <= (40LL << 20)) cw = 64;
     }
     while (cw > 32 && geo.nb % cw) cw >>= 1;
     if (cw < 32 || geo.nb % cw) return -1;
