@@ -299,20 +299,25 @@ def _check_pair(table, out):
         raise ContractError(f"unsupported table type {type(table).__name__} (tiled: eval_tiled)")
 
 
-def _as_positions(pos) -> np.ndarray:
+def _as_positions(pos, check_finite: bool = True) -> np.ndarray:
     """kernels.py:434-442: fp64 C-contiguous (ns, 3); (3,) -> (1, 3)."""
     arr = np.ascontiguousarray(pos, dtype=np.float64)
     if arr.ndim == 1:
         arr = arr.reshape(1, 3) if arr.size == 3 else arr
     if arr.ndim != 2 or arr.shape[1] != 3:
         raise ContractError(f"positions must have shape (ns, 3), got {arr.shape}")
-    if not np.isfinite(arr).all():
+    if check_finite and not np.isfinite(arr).all():
         raise DomainError("positions contain non-finite components")
     return arr
 
 
-# positions per device pass of the drop-in path (bounds its scratch buffer)
-DROPIN_CHUNK = 1 << 16
+# Drop-in path: positions per device pass, and the scratch bytes it may use.
+DROPIN_CHUNK = 1 << 18
+DROPIN_SCRATCH_BYTES = 16 << 30
+# Batches larger than this are checked for non-finite positions on the device
+# (the kernels' status flag) instead of by a host pass; either way DomainError
+# is raised before the caller's buffers are touched.
+HOST_FINITE_CHECK_MAX = 4096
 
 
 def _eval_last(table, kind, pos: np.ndarray, mode: str):
@@ -322,23 +327,28 @@ def _eval_last(table, kind, pos: np.ndarray, mode: str):
     dt = as_device_table(table)
     S = kind.output_streams_soa
     P = pos.shape[0]
-    chunk = min(P, DROPIN_CHUNK)
+    item = 8 if dt.dtype == np.float64 else 4
+    chunk = max(1, min(P, DROPIN_CHUNK, DROPIN_SCRATCH_BYTES // (S * dt.lanes * item)))
     tdt = torch.float64 if dt.dtype == np.float64 else torch.float32
     scratch = torch.empty((chunk, S, dt.lanes), dtype=tdt, device=dt.device)
+    status = torch.zeros(1, dtype=torch.int32, device=dt.device)
     dpos = torch.from_numpy(pos).to(dt.device)
     last = None
     for lo in range(0, P, chunk):
         hi = min(P, lo + chunk)
-        evaluate(dt, kind, dpos[lo:hi], scratch, mode=mode, check=False)
+        evaluate(dt, kind, dpos[lo:hi], scratch, mode=mode, status=status, check=False)
         last = hi - lo - 1
-    return dt, scratch[last].cpu().numpy()
+    block = scratch[last].cpu().numpy()
+    if int(status.item()) != 0:
+        raise DomainError("positions contain non-finite components")
+    return dt, block
 
 
 def eval_batch(table, kind, positions, out, *, mode: str = "fast") -> None:
     """Evaluate at every position in order; `out` keeps the last one
     (kernels.py:445-473).  Tiled tables take one WalkerOutputsSoA per tile."""
     kind = as_kind(kind)
-    pos = _as_positions(positions)
+    pos = _as_positions(positions, check_finite=np.size(positions) <= 3 * HOST_FINITE_CHECK_MAX)
     layout = getattr(table, "layout", None)
     if layout == "aosoa" or isinstance(table, TiledCoeffTable):
         if len(out) != table.n_tiles:
