@@ -32,6 +32,28 @@ inline int ok() {
     return SPO_OK;
 }
 
+// The library links its own static CUDA runtime, whose current device is
+// independent of the caller's (torch's) runtime.  Before launching, make it
+// follow the device that owns the buffer the launch writes.
+inline int bind_device(const void *ptr) {
+    if (!ptr) return SPO_OK;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SPO_ERR_CONTRACT, "pointer %p is not a CUDA allocation", ptr);
+    }
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+        return fail(SPO_ERR_CONTRACT, "pointer %p is not device memory", ptr);
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != at.device) {
+        if (cudaSetDevice(at.device) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(SPO_ERR_CUDA, "cudaSetDevice(%d) failed", at.device);
+        }
+    }
+    return SPO_OK;
+}
+
 inline int check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SPO_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));

@@ -341,6 +341,8 @@ extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const 
         if (!(dinv3[ax] > 0.0) || !(delta3[ax] > 0.0))
             return fail(SPO_ERR_CONFIG, "grid spacing on axis %d must be positive", ax);
 
+    rc = bind_device(out);
+    if (rc) return rc;
     if (dtype == SPO_F32 && mode == SPO_MODE_FAST) {
         static const char *env_tma = getenv("SPO_TMA");
         static const char *env_cw = getenv("SPO_CW");

@@ -50,6 +50,8 @@ extern "C" int spo_basis_weights(int dtype, const double *t, int64_t n, double d
     if (n == 0) return ok();
     if (!t || !w) return fail(SPO_ERR_CONTRACT, "NULL pointer");
     if (!(dinv > 0.0) || !(delta > 0.0)) return fail(SPO_ERR_DOMAIN, "spacing must be positive");
+    int rc = bind_device(w);
+    if (rc) return rc;
     long long blocks = (n + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -77,6 +79,8 @@ extern "C" int spo_prologue(int dtype, const int32_t *n3, const double *dinv3, c
         g.delta[ax] = delta3[ax];
         g.n[ax] = n3[ax];
     }
+    int rc = bind_device(pos);
+    if (rc) return rc;
     long long blocks = (n_pos + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

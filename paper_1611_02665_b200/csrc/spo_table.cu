@@ -190,6 +190,8 @@ extern "C" int spo_pack_table(int dtype, const void *src, int32_t src_npad, int3
     if (rc) return rc;
     if (!src || !dst) return fail(SPO_ERR_CONTRACT, "NULL table pointer");
     if (src_npad < n_splines) return fail(SPO_ERR_CONTRACT, "src_npad=%d < n_splines=%d", src_npad, n_splines);
+    rc = bind_device(dst);
+    if (rc) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (dtype == SPO_F64)
         pack_kernel<double><<<grid_for(g.total), 256, 0, st>>>((const double *)src, src_npad, g, (double *)dst);
@@ -205,6 +207,8 @@ extern "C" int spo_fill_uniform(const uint64_t *keys, int32_t n_splines, const i
     int rc = make_pack_geom(SPO_F32, n_splines, n3, tile_size, nb, n_tiles, &g);
     if (rc) return rc;
     if (!keys || !dst) return fail(SPO_ERR_CONTRACT, "NULL pointer");
+    rc = bind_device(dst);
+    if (rc) return rc;
     fill_uniform_kernel<<<grid_for(g.total), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
         reinterpret_cast<const unsigned long long *>(keys), g, dst);
     return check_launch("spo_fill_uniform");
@@ -217,6 +221,8 @@ extern "C" int spo_fill_normal_f64(const uint64_t *keys, int32_t n_splines, cons
     int rc = make_pack_geom(SPO_F64, n_splines, n3, tile_size, nb, n_tiles, &g);
     if (rc) return rc;
     if (!keys || !dst) return fail(SPO_ERR_CONTRACT, "NULL pointer");
+    rc = bind_device(dst);
+    if (rc) return rc;
     fill_normal_kernel<<<grid_for(g.total), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
         reinterpret_cast<const unsigned long long *>(keys), g, dst);
     return check_launch("spo_fill_normal_f64");
@@ -228,6 +234,8 @@ extern "C" int spo_fill_positions(uint64_t seed, int64_t walker0, int64_t n_walk
     if (n_walkers < 0 || ns < 0) return fail(SPO_ERR_CONTRACT, "negative walker or sample count");
     if (n_walkers == 0 || ns == 0) return ok();
     if (!out || !lengths3) return fail(SPO_ERR_CONTRACT, "NULL pointer");
+    const int rc = bind_device(out);
+    if (rc) return rc;
     const long long total = n_walkers * ns * 3;
     positions_kernel<<<grid_for(total), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
         seed, walker0, n_walkers, iteration, kernel_id, ns, lengths3[0], lengths3[1], lengths3[2], out);
