@@ -47,6 +47,7 @@ struct Args {
     long long out_pos_stride, out_stream_stride;
     const long long *out_index;
     int evict_last;           // L2 evict_last hint on table slabs
+    int proxy_fence;          // fence.proxy.async before reusing a stage (diagnostic)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
                 it.b0 = b * BP;
                 it.nb = (int)min((long long)BP, a.n_pos - it.b0);
                 it.G = (it.nb + PW - 1) / PW;
-                fence_proxy_async();  // generic reads of this slot precede the async write
+                if (a.proxy_fence) fence_proxy_async();  // WAR on the slot, see issue()
                 mbar_arrive_expect_tx(&rbar[slot], (unsigned)(it.nb * REC * 4));
                 bulk_load(recs + slot * BP * REC, a.recs + it.b0 * REC, (unsigned)(it.nb * REC * 4), &rbar[slot]);
             } else {
@@ -351,7 +352,10 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
     // lane 0: issue slab ii of the described group into stage st
     auto issue = [&](const GroupDesc<PW> &d, int ii, int st, unsigned long long policy) {
         unsigned char *dst = ring + st * STAGE;
-        fence_proxy_async();
+        // WAR only (LDS reads of this stage, all consumed before the
+        // __syncwarp above, then the TMA write): no proxy fence needed, as in
+        // a consumer-release / producer-acquire TMA pipeline.
+        if (a.proxy_fence) fence_proxy_async();
         mbar_arrive_expect_tx(&bars[st], d.bytes);
 #pragma unroll
         for (int q = 0; q < PW; ++q)
@@ -569,6 +573,8 @@ int eval_tma(int kind, const float *table, const TableGeom &geo, const GridArgs 
     a.out_index = out_index;
     static const char *env_hint = getenv("SPO_L2HINT");
     a.evict_last = !(env_hint && env_hint[0] == '0');
+    static const char *env_fence = getenv("SPO_PROXY_FENCE");
+    a.proxy_fence = env_fence && env_fence[0] == '1';
     if (a.n_items >= (1LL << 32)) return -1;  // 32-bit ticket counter
 
     int dev = 0, sms = 148;
