@@ -194,8 +194,13 @@ def _positions_tensor(positions, device):
     return torch.from_numpy(arr).to(device)
 
 
+# positions x lanes from which the TMA-pipelined kernel beats the generic one
+# (scripts/micro/small_batch.py: crossover ~2^20 for N = 64 ... 4096)
+PIPELINE_MIN_WORK = 1 << 20
+
+
 def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=None,
-             status=None, check: bool = True, pipeline: bool = True):
+             status=None, check: bool = True, pipeline="auto"):
     """Evaluate `kind` at every position; returns out[P][S][lanes] (CUDA).
 
     table      DeviceTable (or any host table -> uploaded once and cached)
@@ -206,7 +211,8 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
     status     optional int32 CUDA tensor(1): set to 1 on a non-finite position
     check      raise DomainError for non-finite positions (one sync on status)
     pipeline   fp32 fast mode: True = TMA-pipelined kernel (needs a workspace,
-               allocated here), False = the generic kernel (same bits)
+               allocated here), False = the generic kernel (same bits),
+               "auto" = pipelined when P * lanes >= PIPELINE_MIN_WORK
     """
     torch = _torch()
     kind = as_kind(kind)
@@ -239,6 +245,8 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
         idx_ptr = out_index.contiguous().data_ptr()
     g = dt.grid
     L = _abi.load()
+    if pipeline == "auto":  # small batches: one generic launch beats prologue + TMA setup
+        pipeline = P * dt.lanes >= PIPELINE_MIN_WORK
     ws_bytes = int(L.spo_eval_workspace_bytes(kind.code, dt.dtype_code, _MODES[mode], P)) if pipeline else 0
     ws = torch.empty(max(ws_bytes, 0), dtype=torch.uint8, device=device) if ws_bytes > 0 else None
     _abi.check(L.spo_eval(

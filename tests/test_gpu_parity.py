@@ -39,8 +39,8 @@ def cfg1(torch):
     return host, DeviceTable.from_host(host)
 
 
-def run(dt, kind, pos, mode="fast", n=None):
-    out = evaluate(dt, kind, pos, mode=mode)
+def run(dt, kind, pos, mode="fast", pipeline="auto"):
+    out = evaluate(dt, kind, pos, mode=mode, pipeline=pipeline)
     s = streams(out, dt, kind)
     names = KernelKind(kind).stream_names
     return np.stack([s[k].cpu().numpy() for k in names], axis=1)
@@ -105,11 +105,12 @@ def test_device_fill_tiled_and_ragged(torch, golden_small):
 
 # -------------------------------------------------------------- config 1 --
 
+@pytest.mark.parametrize("pipeline", [True, False])
 @pytest.mark.parametrize("kind", KINDS)
-def test_cfg1_fast_within_tolerance(cfg1, golden_cfg1, kind):
+def test_cfg1_fast_within_tolerance(cfg1, golden_cfg1, kind, pipeline):
     host, dt = cfg1
     pos = golden_cfg1["positions"]
-    got = run(dt, kind, pos)
+    got = run(dt, kind, pos, pipeline=pipeline)
     ref, scale = oracle.eval_f64(kind, host.data, 64, host.grid.spacings, pos)
     ok, worst = oracle.tolerance_check(got, ref, scale, TOL32)
     assert ok, worst
@@ -199,8 +200,9 @@ def test_small_cases(torch, golden_small, tag):
     for kind in KINDS:
         np.testing.assert_array_equal(run(dt, kind, pos, "strict"), golden_small[f"{tag}_{kind}_f32"])
         ref, scale = oracle.eval_f64(kind, host.data, n, spac, pos)
-        ok, worst = oracle.tolerance_check(run(dt, kind, pos), ref, scale, TOL32)
-        assert ok, (kind, worst)
+        for pipeline in (True, False):
+            ok, worst = oracle.tolerance_check(run(dt, kind, pos, pipeline=pipeline), ref, scale, TOL32)
+            assert ok, (kind, pipeline, worst)
 
 
 def test_out_index_scatter_is_bitwise(torch, cfg1, golden_cfg1):
@@ -223,10 +225,13 @@ def test_nonfinite_positions_raise(torch, cfg1):
     dpos = torch.tensor([[0.1, 0.2, 0.3], [0.0, np.inf, 0.0]], dtype=torch.float64, device="cuda")
     with pytest.raises(DomainError):
         evaluate(dt, "vgh", dpos)
-    status = torch.zeros(1, dtype=torch.int32, device="cuda")
-    out = evaluate(dt, "vgh", dpos, status=status, check=False)
-    assert int(status.item()) == 1
-    assert torch.isnan(out[1]).all() and torch.isfinite(out[0]).all()
+    for pipeline in (True, False):
+        with pytest.raises(DomainError):
+            evaluate(dt, "vgh", dpos, pipeline=pipeline)
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        out = evaluate(dt, "vgh", dpos, status=status, check=False, pipeline=pipeline)
+        assert int(status.item()) == 1
+        assert torch.isnan(out[1]).all() and torch.isfinite(out[0]).all()
 
 
 # ---------------------------------------------------------------- fp64 --
