@@ -367,6 +367,7 @@ def run_b200(args):
 
     if rank == 0 and not args.no_e2e:
         result["e2e"] = e2e_dropin(table, kind, pos_np, N, S, eval_batch, WalkerOutputsSoA, args, dev)
+        result["e2e_full_outputs"] = e2e_full_outputs(table, kind, pos_np, N, S, dev)
     if world > 1:
         import torch.distributed as dist
 
@@ -383,6 +384,46 @@ def run_b200(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def e2e_full_outputs(table, kind, pos_np, N, S, dev, chunk=8192, seconds=2.0):
+    """Transparency figure: the same metric when EVERY output is copied back to
+    pinned host memory (H2D positions + kernel + D2H of all [P][S][N] outputs,
+    double-buffered over two streams).  PCIe-bound by construction; measured on
+    a bounded sample of the workload's positions."""
+    import torch
+
+    from paper_1611_02665_b200 import evaluate
+
+    pin_pos = torch.from_numpy(pos_np).pin_memory()
+    host = [torch.empty((chunk, S, table.lanes), dtype=torch.float32).pin_memory() for _ in range(2)]
+    dout = [torch.empty((chunk, S, table.lanes), dtype=torch.float32, device=dev) for _ in range(2)]
+    dpos = [torch.empty((chunk, 3), dtype=torch.float64, device=dev) for _ in range(2)]
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    n_chunks = max(2, min(len(pos_np) // chunk, 64))
+    done = [torch.cuda.Event() for _ in range(2)]
+
+    def run(k):
+        b = k & 1
+        with torch.cuda.stream(streams[b]):
+            done[b].synchronize()
+            dpos[b].copy_(pin_pos[k * chunk:(k + 1) * chunk], non_blocking=True)
+            evaluate(table, kind, dpos[b], dout[b], check=False)
+            host[b].copy_(dout[b], non_blocking=True)
+            done[b].record(streams[b])
+
+    run(0)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    k = 0
+    while k < n_chunks and (time.perf_counter() - t0 < seconds or k < 2):
+        run(k)
+        k += 1
+    torch.cuda.synchronize(dev)
+    dt = time.perf_counter() - t0
+    return {"value": k * chunk * N / dt, "unit": UNIT, "h2d_bytes_per_step": int(k * chunk * 24),
+            "d2h_bytes_per_step": int(k * chunk * S * table.lanes * 4),
+            "sample": f"{k} chunks of {chunk} positions, all outputs to pinned host memory"}
 
 
 def e2e_dropin(table, kind, pos_np, N, S, eval_batch, WalkerOutputsSoA, args, dev):
