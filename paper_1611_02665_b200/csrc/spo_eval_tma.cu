@@ -33,7 +33,7 @@ namespace tma {
 
 constexpr int STAGE = 8192;   // bytes: 128 fp32 lanes x 16 rows
 constexpr int REC = 40;       // floats per position record: 36 weights, i0, j0, k0, pad
-constexpr int WS_HEADER = 256;
+constexpr int WS_HEADER = 1024;  // ticket @0, bucket counts @256, bucket cursors @512
 
 struct Args {
     const float *recs;        // [n_pos][REC]
@@ -224,30 +224,89 @@ __device__ __forceinline__ void slab_fma(const float *__restrict__ slab, const f
 }
 
 // ------------------------------------------------------------ prologue --
-__global__ void prologue_records_kernel(GridArgs g, const double *__restrict__ pos, long long n,
-                                        float *__restrict__ recs, int *__restrict__ status) {
+// Positions are binned by the spatial block (NBK^3 blocks of the grid) of
+// their stencil cell, so that the eval kernel's unit-major sweep touches one
+// block's rows at a time: the L2 working set is (rows / NBK^3) x CW x 4 B,
+// small enough for CW = 128 (one TMA per position-slab instead of four).
+constexpr int NBK = 4;
+constexpr int NBUCKET = NBK * NBK * NBK;
+
+__device__ __forceinline__ int bucket_of_cell(int i0, int j0, int k0, const GridArgs &g) {
+    if (i0 < 0) return 0;
+    const int bi = i0 * NBK / g.n[0], bj = j0 * NBK / g.n[1], bk = k0 * NBK / g.n[2];
+    return (bi * NBK + bj) * NBK + bk;
+}
+
+// pass 1: bucket of every position + bucket histogram (block-aggregated)
+__global__ void bucket_count_kernel(GridArgs g, const double *__restrict__ pos, long long n,
+                                    unsigned char *__restrict__ bucket, unsigned *__restrict__ counts) {
+    __shared__ unsigned hist[NBUCKET];
+    for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
          p += (long long)gridDim.x * blockDim.x) {
+        double t;
         const double x = pos[3 * p], y = pos[3 * p + 1], z = pos[3 * p + 2];
-        double tx, ty, tz;
-        int i0 = map_axis(x, g.dinv[0], g.cnt[0], &tx);
-        const int j0 = map_axis(y, g.dinv[1], g.cnt[1], &ty);
-        const int k0 = map_axis(z, g.dinv[2], g.cnt[2], &tz);
-        float w[REC];
-        weights_f32(tx, g.dinv[0], w);
-        weights_f32(ty, g.dinv[1], w + 12);
-        weights_f32(tz, g.dinv[2], w + 24);
-        if (!(isfinite(x) && isfinite(y) && isfinite(z))) {
-            if (status) atomicOr(status, 1);
-            i0 = -1;
+        int i0 = map_axis(x, g.dinv[0], g.cnt[0], &t);
+        const int j0 = map_axis(y, g.dinv[1], g.cnt[1], &t);
+        const int k0 = map_axis(z, g.dinv[2], g.cnt[2], &t);
+        if (!(isfinite(x) && isfinite(y) && isfinite(z))) i0 = -1;
+        const int b = bucket_of_cell(i0, j0, k0, g);
+        bucket[p] = (unsigned char)b;
+        atomicAdd(&hist[b], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x)
+        if (hist[b]) atomicAdd(&counts[b], hist[b]);
+}
+
+// pass 2: records (bit-exact mapping + 36 fp32 weights + cell + original
+// index) scattered to their bucket's range; slots are reserved per block.
+__global__ void prologue_records_kernel(GridArgs g, const double *__restrict__ pos, long long n,
+                                        const unsigned char *__restrict__ bucket,
+                                        const unsigned *__restrict__ counts, unsigned *__restrict__ cursors,
+                                        float *__restrict__ recs, int *__restrict__ status) {
+    __shared__ unsigned offs[NBUCKET], local[NBUCKET], base[NBUCKET];
+    if (threadIdx.x == 0) {
+        unsigned s = 0;
+        for (int b = 0; b < NBUCKET; ++b) {
+            offs[b] = s;
+            s += counts[b];
         }
-        w[36] = __int_as_float(i0);
-        w[37] = __int_as_float(j0);
-        w[38] = __int_as_float(k0);
-        w[39] = 0.0f;
-        float4 *dst = reinterpret_cast<float4 *>(recs + p * REC);
+    }
+    for (long long p0 = blockIdx.x * (long long)blockDim.x; p0 < n; p0 += (long long)gridDim.x * blockDim.x) {
+        const long long p = p0 + threadIdx.x;
+        for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x) local[b] = 0;
+        __syncthreads();
+        const int b = p < n ? bucket[p] : 0;
+        const unsigned rank = p < n ? atomicAdd(&local[b], 1u) : 0u;
+        __syncthreads();
+        for (int q = threadIdx.x; q < NBUCKET; q += blockDim.x)
+            base[q] = local[q] ? offs[q] + atomicAdd(&cursors[q], local[q]) : 0u;
+        __syncthreads();
+        if (p < n) {
+            const double x = pos[3 * p], y = pos[3 * p + 1], z = pos[3 * p + 2];
+            double tx, ty, tz;
+            int i0 = map_axis(x, g.dinv[0], g.cnt[0], &tx);
+            const int j0 = map_axis(y, g.dinv[1], g.cnt[1], &ty);
+            const int k0 = map_axis(z, g.dinv[2], g.cnt[2], &tz);
+            float w[REC];
+            weights_f32(tx, g.dinv[0], w);
+            weights_f32(ty, g.dinv[1], w + 12);
+            weights_f32(tz, g.dinv[2], w + 24);
+            if (!(isfinite(x) && isfinite(y) && isfinite(z))) {
+                if (status) atomicOr(status, 1);
+                i0 = -1;
+            }
+            w[36] = __int_as_float(i0);
+            w[37] = __int_as_float(j0);
+            w[38] = __int_as_float(k0);
+            w[39] = __int_as_float((int)p);  // original position index
+            float4 *dst = reinterpret_cast<float4 *>(recs + (long long)(base[b] + rank) * REC);
 #pragma unroll
-        for (int e = 0; e < REC / 4; ++e) dst[e] = make_float4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+            for (int e = 0; e < REC / 4; ++e) dst[e] = make_float4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+        }
+        __syncthreads();
     }
 }
 
@@ -442,7 +501,7 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
                 st ^= 1;
             }
             if (p < it.nb) {
-                const long long gp = it.b0 + p;
+                const long long gp = __float_as_int(rc[p * REC + 39]);  // original index
                 const long long op = a.out_index ? a.out_index[gp] : gp;
                 float *o = a.out + op * a.out_pos_stride + (long long)it.m * a.nb + it.c * CW + vl * 4;
 #pragma unroll
@@ -511,7 +570,11 @@ static int launch_cw(int cw, const CUtensorMap &map, const Args &a, int sms, cud
 
 }  // namespace tma
 
-long long eval_tma_workspace_bytes(long long n_pos) { return tma::WS_HEADER + n_pos * tma::REC * 4; }
+// workspace: [header: ticket | bucket counts | bucket cursors] [bucket id per
+// position, 16-byte padded] [records, bucket-sorted]
+long long eval_tma_workspace_bytes(long long n_pos) {
+    return tma::WS_HEADER + ((n_pos + 15) / 16) * 16 + n_pos * tma::REC * 4;
+}
 
 
 // Called by spo_eval for fp32 FAST requests with a workspace.  Returns -1
@@ -529,8 +592,8 @@ int eval_tma(int kind, const float *table, const TableGeom &geo, const GridArgs 
     int cw = cw_request;
     if (cw == 0) {
         cw = 32;
-        if (rows * 128 * 4 <= (40LL << 20)) cw = 128;
-        else if (rows * 64 * 4 <= (40LL << 20)) cw = 64;
+        if (rows * 128 * 4 / NBUCKET <= (40LL << 20)) cw = 128;
+        else if (rows * 64 * 4 / NBUCKET <= (40LL << 20)) cw = 64;
     }
     while (cw > 32 && geo.nb % cw) cw >>= 1;
     if (cw < 32 || geo.nb % cw) return -1;
@@ -547,13 +610,19 @@ int eval_tma(int kind, const float *table, const TableGeom &geo, const GridArgs 
                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
 
+    if (n_pos >= (1LL << 31)) return -1;  // records carry 32-bit original indices
     unsigned char *ws = static_cast<unsigned char *>(workspace);
-    float *recs = reinterpret_cast<float *>(ws + WS_HEADER);
+    unsigned *counts = reinterpret_cast<unsigned *>(ws + 256);
+    unsigned *cursors = reinterpret_cast<unsigned *>(ws + 512);
+    unsigned char *bucket = ws + WS_HEADER;
+    float *recs = reinterpret_cast<float *>(ws + WS_HEADER + ((n_pos + 15) / 16) * 16);
     if (cudaMemsetAsync(ws, 0, WS_HEADER, st) != cudaSuccess) return check_launch("workspace reset");
     {
         long long blocks = (n_pos + 255) / 256;
         if (blocks > 148LL * 16) blocks = 148LL * 16;
-        prologue_records_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, recs, status);
+        bucket_count_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, bucket, counts);
+        prologue_records_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, bucket, counts, cursors, recs,
+                                                                  status);
         int rc = check_launch("spo_eval (prologue) launch");
         if (rc) return rc;
     }

@@ -43,6 +43,7 @@ def _round_up(n: int, q: int) -> int:
 # L2 working-set target for one AoSoA tile slice: B200 caches per die (2 x ~63 MB),
 # and the next unit plus the output stream share it (measured: 40 MB beats 80 MB).
 TILE_SLICE_BYTES = 40 << 20
+SPATIAL_BUCKETS = 64  # csrc/spo_eval_tma.cu NBUCKET (4 x 4 x 4 blocks)
 
 
 def auto_tile_size(grid: GridSpec, n_splines: int, dtype=np.float32):
@@ -54,8 +55,11 @@ def auto_tile_size(grid: GridSpec, n_splines: int, dtype=np.float32):
     item = np.dtype(dtype).itemsize
     q = lane_quantum(dtype)
     tile = q
+    # fp32 goes through the TMA kernel, which also bins positions into
+    # SPATIAL_BUCKETS blocks of the grid: its working set is a block's rows
+    buckets = SPATIAL_BUCKETS if np.dtype(dtype) == np.float32 else 1
     for cand in (128, 64, 32):
-        if cand % q == 0 and rows * cand * item <= TILE_SLICE_BYTES:
+        if cand % q == 0 and rows * cand * item // buckets <= TILE_SLICE_BYTES:
             tile = cand
             break
     if n_splines <= tile:
