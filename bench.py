@@ -336,7 +336,8 @@ def run_b200(args):
 
     pipelined = args.mode == "fast" and _abi.load().spo_eval_workspace_bytes(
         KernelKind(kind).code, 0, 0, chunk) > 0
-    kernels_per_call = 2 if pipelined else 1  # prologue_records_kernel + eval_tma_kernel
+    # bucket_count_kernel + prologue_records_kernel + eval_tma_kernel
+    kernels_per_call = 3 if pipelined else 1
     kernel_name = (f"spo::tma::eval_tma_kernel<{kind.upper()}> (+ prologue_records_kernel, timed together)"
                    if pipelined else f"spo::eval_kernel<{kind.upper()},float,{args.mode}>")
     peak, peak_src = measured_peak()
