@@ -255,3 +255,47 @@ def test_fp64_normal_fill_moments(torch):
     dt = DeviceTable.normal_f64(unit_cell_grid(16), 64, seed=0)
     v = dt.reference_soa()[..., :64].reshape(-1)
     assert abs(v.mean()) < 0.01 and abs(v.std() - 1.0) < 0.01
+
+
+# ------------------------------------------------------- edge cases --
+
+def test_pipelined_edge_cases(torch, golden_mapping):
+    """The TMA path on awkward inputs: huge / negative / boundary coordinates,
+    a ragged tiled table (tile 24 -> 32-lane rows), strided output views,
+    out_index scatter, P = 1 and P = 0, two streams at once."""
+    grid = GridSpec(20, 24, 28, 0.05, 1 / 24, 1 / 28)
+    host = build_table(grid, 72, FillSpec.random(11))
+    xs = golden_mapping["xs"]
+    rng = np.random.default_rng(3)
+    pos = np.stack([rng.choice(xs, 3000), rng.choice(xs, 3000), rng.random(3000)], axis=1)
+    ref_dt = DeviceTable.from_host(host, tile_size=None)
+    base = evaluate(ref_dt, "vgh", pos, pipeline=False)
+    for tile in (None, 24, 32):
+        dt = DeviceTable.from_host(host, tile_size=tile)
+        got = streams(evaluate(dt, "vgh", pos, pipeline=True), dt, "vgh")
+        want = streams(base, ref_dt, "vgh")
+        for k in want:
+            assert torch.equal(got[k], want[k]), (tile, k)
+    ref, scale = oracle.eval_f64("vgh", host.data, 72, grid.spacings, pos[:200])
+    ok, worst = oracle.tolerance_check(run(ref_dt, "vgh", pos[:200], pipeline=True), ref, scale, TOL32)
+    assert ok, worst
+    # strided output view + out_index scatter
+    big = torch.zeros((3000, 10, 256), dtype=torch.float32, device="cuda")
+    view = big[:, :, 64:64 + ref_dt.lanes]
+    perm = rng.permutation(3000)
+    evaluate(ref_dt, "vgh", pos[perm], view, out_index=torch.from_numpy(perm).cuda(), pipeline=True)
+    assert torch.equal(view, base) and (big[:, :, :64] == 0).all()
+    # tiny and empty batches
+    one = evaluate(ref_dt, "vgh", pos[:1], pipeline=True)
+    assert torch.equal(one[0], base[0])
+    empty = evaluate(ref_dt, "vgh", np.zeros((0, 3)), pipeline=True)
+    assert empty.shape[0] == 0
+    # two streams concurrently (separate workspaces and tickets)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(s1):
+        a = evaluate(ref_dt, "vgh", pos, pipeline=True, check=False)
+    with torch.cuda.stream(s2):
+        b = evaluate(ref_dt, "vgl", pos, pipeline=True, check=False)
+    torch.cuda.synchronize()
+    assert torch.equal(a, base)
+    assert torch.equal(b[:, :4], base[:, :4])
