@@ -290,10 +290,10 @@ static int launch(const EvalArgs &a, dim3 grid, dim3 block, size_t smem, cudaStr
 }  // namespace spo
 
 namespace spo {
-int eval_tma(int kind, const float *table, const TableGeom &geo, const GridArgs &g, const double *pos,
-             long long n_pos, float *out, long long ops, long long oss, const long long *out_index, int *status,
+int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const GridArgs &g, const double *pos,
+             long long n_pos, void *out, long long ops, long long oss, const long long *out_index, int *status,
              void *workspace, long long ws_bytes, cudaStream_t st, int cw_request);
-long long eval_tma_workspace_bytes(long long n_pos);
+long long eval_tma_workspace_bytes(int dtype, long long n_pos);
 }
 
 using namespace spo;
@@ -304,8 +304,8 @@ extern "C" const char *spo_last_error(void) { return last_error_slot().c_str(); 
 
 extern "C" int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64_t n_pos) {
     if (kind < SPO_KIND_V || kind > SPO_KIND_VGH || n_pos < 0) return -1;
-    if (dtype != SPO_F32 || mode != SPO_MODE_FAST) return 0;
-    return eval_tma_workspace_bytes(n_pos);
+    if ((dtype != SPO_F32 && dtype != SPO_F64) || mode != SPO_MODE_FAST) return 0;
+    return eval_tma_workspace_bytes(dtype, n_pos);
 }
 
 extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const int32_t *n3,
@@ -343,7 +343,7 @@ extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const 
 
     rc = bind_device(out);
     if (rc) return rc;
-    if (dtype == SPO_F32 && mode == SPO_MODE_FAST) {
+    if (mode == SPO_MODE_FAST) {
         static const char *env_tma = getenv("SPO_TMA");
         static const char *env_cw = getenv("SPO_CW");
         if (!(env_tma && env_tma[0] == '0')) {
@@ -354,8 +354,7 @@ extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const 
                 g.delta[ax] = delta3[ax];
                 g.n[ax] = n3[ax];
             }
-            const int r = eval_tma(kind, static_cast<const float *>(table), geo, g, pos, n_pos,
-                                   static_cast<float *>(out), out_pos_stride, out_stream_stride,
+            const int r = eval_tma(kind, dtype, table, geo, g, pos, n_pos, out, out_pos_stride, out_stream_stride,
                                    reinterpret_cast<const long long *>(out_index), status, workspace,
                                    workspace_bytes, reinterpret_cast<cudaStream_t>(stream),
                                    env_cw ? atoi(env_cw) : 0);

@@ -1,26 +1,29 @@
-// spo_eval_tma.cu -- TMA-pipelined fp32 V / VGL / VGH kernel (the fast path).
+// spo_eval_tma.cu -- TMA-pipelined V / VGL / VGH kernels (the fast path, fp32
+// and fp64).
 //
 // Same math as spo_eval.cu's separable FAST contraction (kernels.py:143-247
-// restated as k-, then j-, then i-sums with FMA), different data movement.
+// restated as k-, then j-, then i-sums with FMA, bitwise the same sequence),
+// different data movement:
 //
-//  1. prologue_records_kernel: one thread per position maps it to (i0,j0,k0)
-//     and the 36 fp32 basis weights, bit-exactly (spo_prologue.cuh), into a
-//     160-byte record in the caller's workspace.  Once per position per call.
-//  2. eval_tma_kernel: persistent CTAs (one per SM) of 8 warps.  Work items
-//     are (unit u = (tile m, chunk c of CW lanes), batch of BP positions) and
-//     are handed out by a global ticket counter in unit-major order, so at any
-//     moment the whole GPU works on one or two units: the L2 working set is one
-//     CW-wide slice of the table (rows x CW x 4 B, 38.5 MB for 67^3 at CW = 32)
-//     -- the paper's AoSoA cache blocking, enforced by scheduling rather than by
-//     hoping CTAs stay in step.
-//     Per warp, a ring of R stages is fed by TMA: one cp.async.bulk.tensor.5d
-//     per (position, i) brings the 4(j) x 4(k) x CW slab (16 rows) into shared
-//     memory and completes on the stage's mbarrier; item records arrive by a
-//     cp.async.bulk copy on their own mbarriers (double-buffered).  The warp
-//     runs R-1 slabs ahead of its compute, across item boundaries.
-//     Compute: lane = (position in group, 16-byte lane vector), 4 orbitals per
-//     lane, S accumulators per orbital kept in registers over the 4 i-slabs,
-//     streaming 16-byte stores.
+//  1. bucket_count_kernel + prologue_records_kernel: one thread per position
+//     maps it to (i0,j0,k0) and its 36 basis weights (fp32: bit-exact grid.py
+//     form; fp64: oracle.py form) into a record carrying the cell and the
+//     original index, counting-sorted into 4x4x4 spatial blocks of the grid.
+//  2. eval_tma_kernel: persistent CTAs (one per SM).  Work items are (unit u =
+//     (tile m, chunk c of CW lanes), batch of BP bucket-sorted positions),
+//     handed out by a global ticket counter in unit-major order, so at any
+//     moment the GPU works on one CW-wide slice of the table and, inside it,
+//     on one spatial block: the L2 working set is a block's rows x CW lanes
+//     (2.4 MB for 67^3 at 128 fp32 lanes) -- the paper's AoSoA cache blocking,
+//     enforced by scheduling.
+//     Per warp, a 2-stage ring of 8 KB shared-memory stages is fed by TMA: one
+//     cp.async.bulk.tensor.5d per (position, i) brings the 4(j) x 4(k) x CW
+//     slab (16 rows) and completes on the stage's mbarrier; item records
+//     arrive by cp.async.bulk on their own mbarriers (double-buffered).  The
+//     warp issues one slab ahead of its compute, across group/item bounds.
+//     Compute: lane = (position in group, 16-byte lane vector: 4 fp32 / 2 fp64
+//     orbitals), S accumulators per orbital in registers over the 4 i-slabs;
+//     fp32 FMAs as packed FFMA2, fp64 as DFMA; 16-byte streaming stores.
 #include <cuda.h>
 
 #include <cstdlib>
@@ -31,23 +34,45 @@
 namespace spo {
 namespace tma {
 
-constexpr int STAGE = 8192;   // bytes: 128 fp32 lanes x 16 rows
-constexpr int REC = 40;       // floats per position record: 36 weights, i0, j0, k0, pad
+constexpr int STAGE = 8192;      // bytes: 32 lanes x 16 B x 16 rows
 constexpr int WS_HEADER = 1024;  // ticket @0, bucket counts @256, bucket cursors @512
 
+// Launch shapes: warps per CTA, ring stages per warp, positions per item.
+template <int WARPS_, int R_, int BP_>
+struct TCfg {
+    static constexpr int WARPS = WARPS_, R = R_, BP = BP_;
+};
+
+template <typename T>
+struct TT;
+template <>
+struct TT<float> {
+    static constexpr int W = 4;                   // elements per 16-byte lane vector
+    static constexpr int RECB = 36 * 4 + 16;      // record bytes: 36 weights + i0 j0 k0 orig
+    using Cfg = TCfg<12, 2, 8>;                   // 160 registers per thread
+};
+template <>
+struct TT<double> {
+    static constexpr int W = 2;
+    static constexpr int RECB = 36 * 8 + 16;
+    // fp64 weights need ~200 registers: 8 warps (2 per SMSP register-file
+    // partition) instead of 12 (3 per partition would cap them at 168)
+    using Cfg = TCfg<8, 2, 8>;
+};
+
 struct Args {
-    const float *recs;        // [n_pos][REC]
+    const unsigned char *recs;  // [n_pos][RECB] bucket-sorted
     unsigned *ticket;
     long long n_pos;
-    long long nbatch;         // ceil(n_pos / BP)
-    long long n_items;        // units * nbatch
-    int chunks;               // chunks of CW lanes per tile row
-    int nb;                   // table row length (lanes)
-    float *out;
+    long long nbatch;           // ceil(n_pos / BP)
+    long long n_items;          // units * nbatch
+    int chunks;                 // chunks of CW lanes per tile row
+    int nb;                     // table row length (lanes)
+    void *out;
     long long out_pos_stride, out_stream_stride;
     const long long *out_index;
-    int evict_last;           // L2 evict_last hint on table slabs
-    int proxy_fence;          // fence.proxy.async before reusing a stage (diagnostic)
+    int evict_last;             // L2 evict_last hint on table slabs
+    int proxy_fence;            // fence.proxy.async before reusing a stage (diagnostic)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -111,6 +136,7 @@ struct NS {
     static constexpr int S = KIND == SPO_KIND_V ? 1 : (KIND == SPO_KIND_VGL ? 5 : 10);
 };
 
+// ----------------------------------------------------------- contraction --
 // Packed fp32x2 FMA (SASS FFMA2, sm_100): two independent round-to-nearest
 // fp32 FMAs per instruction with a broadcast scalar multiplier -- bitwise the
 // same as two __fmaf_rn, at half the issue slots.
@@ -119,11 +145,12 @@ __device__ __forceinline__ float2 fma2(float w, float2 c, float2 acc) {
 }
 __device__ __forceinline__ float2 mul2(float w, float2 c) { return __fmul2_rn(make_float2(w, w), c); }
 
-// slab_fma with the 4 orbitals of a lane handled as two fp32x2 pairs.
+// One i-slab for one lane: 4 fp32 orbitals as two fp32x2 pairs.
+// slab: [j][k][CW] of this lane's position; wy/wz: 12 weights; ax/dax/d2ax: x weights of this i.
 template <int KIND, int CW>
-__device__ __forceinline__ void slab_fma2(const float *__restrict__ slab, const float (&wy)[12],
-                                          const float (&wz)[12], float ax, float dax, float d2ax,
-                                          float2 (&acc)[NS<KIND>::S][2]) {
+__device__ __forceinline__ void slab_contract(const float *__restrict__ slab, const float (&wy)[12],
+                                              const float (&wz)[12], float ax, float dax, float d2ax,
+                                              float2 (&acc)[NS<KIND>::S][2]) {
     float2 t00[2], t10[2], t01[2], t20[2], t11[2], t02[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) t00[h] = t10[h] = t01[h] = t20[h] = t11[h] = t02[h] = make_float2(0.f, 0.f);
@@ -171,63 +198,106 @@ __device__ __forceinline__ void slab_fma2(const float *__restrict__ slab, const 
     }
 }
 
-// One i-slab of the separable contraction for one 16-byte lane vector.
-// slab: [j][k][CW] floats of this lane's position; wy/wz: 12 weights each;
-// ax/dax/d2ax: the x weights of this i.
+// One i-slab for one lane: 2 fp64 orbitals, DFMA in the generic kernel's order.
 template <int KIND, int CW>
-__device__ __forceinline__ void slab_fma(const float *__restrict__ slab, const float (&wy)[12],
-                                         const float (&wz)[12], float ax, float dax, float d2ax,
-                                         float (&acc)[NS<KIND>::S][4]) {
-    float t00[4], t10[4], t01[4], t20[4], t11[4], t02[4];
+__device__ __forceinline__ void slab_contract(const double *__restrict__ slab, const double (&wy)[12],
+                                              const double (&wz)[12], double ax, double dax, double d2ax,
+                                              double2 (&acc)[NS<KIND>::S][1]) {
+    double t00[2], t10[2], t01[2], t20[2], t11[2], t02[2];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) t00[e] = t10[e] = t01[e] = t20[e] = t11[e] = t02[e] = 0.0f;
+    for (int e = 0; e < 2; ++e) t00[e] = t10[e] = t01[e] = t20[e] = t11[e] = t02[e] = 0.0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        float4 c[4];
+        double2 c[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const float4 *>(slab + (j * 4 + k) * CW);
+        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const double2 *>(slab + (j * 4 + k) * CW);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float c0 = (&c[0].x)[e], c1 = (&c[1].x)[e], c2 = (&c[2].x)[e], c3 = (&c[3].x)[e];
-            const float s0 = __fmaf_rn(wz[3], c3, __fmaf_rn(wz[2], c2, __fmaf_rn(wz[1], c1, wz[0] * c0)));
-            t00[e] = __fmaf_rn(wy[j], s0, t00[e]);
+        for (int e = 0; e < 2; ++e) {
+            const double c0 = e ? c[0].y : c[0].x, c1 = e ? c[1].y : c[1].x;
+            const double c2 = e ? c[2].y : c[2].x, c3 = e ? c[3].y : c[3].x;
+            const double s0 = __fma_rn(wz[3], c3, __fma_rn(wz[2], c2, __fma_rn(wz[1], c1, wz[0] * c0)));
+            t00[e] = __fma_rn(wy[j], s0, t00[e]);
             if (KIND != SPO_KIND_V) {
-                const float s1 = __fmaf_rn(wz[7], c3, __fmaf_rn(wz[6], c2, __fmaf_rn(wz[5], c1, wz[4] * c0)));
-                const float s2 = __fmaf_rn(wz[11], c3, __fmaf_rn(wz[10], c2, __fmaf_rn(wz[9], c1, wz[8] * c0)));
-                t10[e] = __fmaf_rn(wy[4 + j], s0, t10[e]);
-                t01[e] = __fmaf_rn(wy[j], s1, t01[e]);
-                t20[e] = __fmaf_rn(wy[8 + j], s0, t20[e]);
-                t02[e] = __fmaf_rn(wy[j], s2, t02[e]);
-                if (KIND == SPO_KIND_VGH) t11[e] = __fmaf_rn(wy[4 + j], s1, t11[e]);
+                const double s1 = __fma_rn(wz[7], c3, __fma_rn(wz[6], c2, __fma_rn(wz[5], c1, wz[4] * c0)));
+                const double s2 = __fma_rn(wz[11], c3, __fma_rn(wz[10], c2, __fma_rn(wz[9], c1, wz[8] * c0)));
+                t10[e] = __fma_rn(wy[4 + j], s0, t10[e]);
+                t01[e] = __fma_rn(wy[j], s1, t01[e]);
+                t20[e] = __fma_rn(wy[8 + j], s0, t20[e]);
+                t02[e] = __fma_rn(wy[j], s2, t02[e]);
+                if (KIND == SPO_KIND_VGH) t11[e] = __fma_rn(wy[4 + j], s1, t11[e]);
             }
         }
     }
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        acc[0][e] = __fmaf_rn(ax, t00[e], acc[0][e]);
+    for (int e = 0; e < 2; ++e) {
+        double *a0 = e ? &acc[0][0].y : &acc[0][0].x;
+        *a0 = __fma_rn(ax, t00[e], *a0);
         if (KIND != SPO_KIND_V) {
-            acc[1][e] = __fmaf_rn(dax, t00[e], acc[1][e]);
-            acc[2][e] = __fmaf_rn(ax, t10[e], acc[2][e]);
-            acc[3][e] = __fmaf_rn(ax, t01[e], acc[3][e]);
+            double *a1 = e ? &acc[1][0].y : &acc[1][0].x;
+            double *a2 = e ? &acc[2][0].y : &acc[2][0].x;
+            double *a3 = e ? &acc[3][0].y : &acc[3][0].x;
+            *a1 = __fma_rn(dax, t00[e], *a1);
+            *a2 = __fma_rn(ax, t10[e], *a2);
+            *a3 = __fma_rn(ax, t01[e], *a3);
         }
-        if (KIND == SPO_KIND_VGL)
-            acc[4][e] = __fmaf_rn(d2ax, t00[e], __fmaf_rn(ax, t20[e], __fmaf_rn(ax, t02[e], acc[4][e])));
+        if (KIND == SPO_KIND_VGL) {
+            double *a4 = e ? &acc[4][0].y : &acc[4][0].x;
+            *a4 = __fma_rn(d2ax, t00[e], __fma_rn(ax, t20[e], __fma_rn(ax, t02[e], *a4)));
+        }
         if (KIND == SPO_KIND_VGH) {
-            acc[4][e] = __fmaf_rn(d2ax, t00[e], acc[4][e]);
-            acc[5][e] = __fmaf_rn(dax, t10[e], acc[5][e]);
-            acc[6][e] = __fmaf_rn(dax, t01[e], acc[6][e]);
-            acc[7][e] = __fmaf_rn(ax, t20[e], acc[7][e]);
-            acc[8][e] = __fmaf_rn(ax, t11[e], acc[8][e]);
-            acc[9][e] = __fmaf_rn(ax, t02[e], acc[9][e]);
+            double *a4 = e ? &acc[4][0].y : &acc[4][0].x;
+            double *a5 = e ? &acc[5][0].y : &acc[5][0].x;
+            double *a6 = e ? &acc[6][0].y : &acc[6][0].x;
+            double *a7 = e ? &acc[7][0].y : &acc[7][0].x;
+            double *a8 = e ? &acc[8][0].y : &acc[8][0].x;
+            double *a9 = e ? &acc[9][0].y : &acc[9][0].x;
+            *a4 = __fma_rn(d2ax, t00[e], *a4);
+            *a5 = __fma_rn(dax, t10[e], *a5);
+            *a6 = __fma_rn(dax, t01[e], *a6);
+            *a7 = __fma_rn(ax, t20[e], *a7);
+            *a8 = __fma_rn(ax, t11[e], *a8);
+            *a9 = __fma_rn(ax, t02[e], *a9);
         }
     }
+}
+
+template <typename T>
+struct Acc;
+template <>
+struct Acc<float> {
+    using V = float2;
+    static constexpr int N = 2;  // two fp32x2 pairs = the lane's 4 orbitals
+};
+template <>
+struct Acc<double> {
+    using V = double2;
+    static constexpr int N = 1;  // one pair = the lane's 2 orbitals
+};
+
+__device__ __forceinline__ void zero(float2 &v) { v = make_float2(0.f, 0.f); }
+__device__ __forceinline__ void zero(double2 &v) { v = make_double2(0.0, 0.0); }
+
+template <int S>
+__device__ __forceinline__ void store_lane(float *o, long long sstride, const float2 (&acc)[S][2], bool finite) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const float4 v = finite ? make_float4(acc[s][0].x, acc[s][0].y, acc[s][1].x, acc[s][1].y)
+                                : make_float4(NAN, NAN, NAN, NAN);
+        __stcs(reinterpret_cast<float4 *>(o + s * sstride), v);
+    }
+}
+template <int S>
+__device__ __forceinline__ void store_lane(double *o, long long sstride, const double2 (&acc)[S][1], bool finite) {
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+        __stcs(reinterpret_cast<double2 *>(o + s * sstride), finite ? acc[s][0] : make_double2(NAN, NAN));
 }
 
 // ------------------------------------------------------------ prologue --
 // Positions are binned by the spatial block (NBK^3 blocks of the grid) of
 // their stencil cell, so that the eval kernel's unit-major sweep touches one
-// block's rows at a time: the L2 working set is (rows / NBK^3) x CW x 4 B,
-// small enough for CW = 128 (one TMA per position-slab instead of four).
+// block's rows at a time: the L2 working set is (rows / NBK^3) x CW lanes,
+// small enough for 512-byte chunks (one TMA per position-slab).
 constexpr int NBK = 4;
 constexpr int NBUCKET = NBK * NBK * NBK;
 
@@ -260,12 +330,24 @@ __global__ void bucket_count_kernel(GridArgs g, const double *__restrict__ pos, 
         if (hist[b]) atomicAdd(&counts[b], hist[b]);
 }
 
-// pass 2: records (bit-exact mapping + 36 fp32 weights + cell + original
-// index) scattered to their bucket's range; slots are reserved per block.
+__device__ __forceinline__ void store_weights(unsigned char *dst, const float (&w)[36]) {
+#pragma unroll
+    for (int e = 0; e < 9; ++e)
+        reinterpret_cast<float4 *>(dst)[e] = make_float4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+}
+__device__ __forceinline__ void store_weights(unsigned char *dst, const double (&w)[36]) {
+#pragma unroll
+    for (int e = 0; e < 18; ++e) reinterpret_cast<double2 *>(dst)[e] = make_double2(w[2 * e], w[2 * e + 1]);
+}
+
+// pass 2: records (bit-exact mapping + 36 weights + cell + original index)
+// scattered to their bucket's range; slots are reserved per block.
+template <typename T>
 __global__ void prologue_records_kernel(GridArgs g, const double *__restrict__ pos, long long n,
                                         const unsigned char *__restrict__ bucket,
                                         const unsigned *__restrict__ counts, unsigned *__restrict__ cursors,
-                                        float *__restrict__ recs, int *__restrict__ status) {
+                                        unsigned char *__restrict__ recs, int *__restrict__ status) {
+    constexpr int RECB = TT<T>::RECB;
     __shared__ unsigned offs[NBUCKET], local[NBUCKET], base[NBUCKET];
     if (threadIdx.x == 0) {
         unsigned s = 0;
@@ -290,34 +372,23 @@ __global__ void prologue_records_kernel(GridArgs g, const double *__restrict__ p
             int i0 = map_axis(x, g.dinv[0], g.cnt[0], &tx);
             const int j0 = map_axis(y, g.dinv[1], g.cnt[1], &ty);
             const int k0 = map_axis(z, g.dinv[2], g.cnt[2], &tz);
-            float w[REC];
-            weights_f32(tx, g.dinv[0], w);
-            weights_f32(ty, g.dinv[1], w + 12);
-            weights_f32(tz, g.dinv[2], w + 24);
+            T w[36];
+            axis_weights<T>(tx, g.dinv[0], g.delta[0], w);
+            axis_weights<T>(ty, g.dinv[1], g.delta[1], w + 12);
+            axis_weights<T>(tz, g.dinv[2], g.delta[2], w + 24);
             if (!(isfinite(x) && isfinite(y) && isfinite(z))) {
                 if (status) atomicOr(status, 1);
                 i0 = -1;
             }
-            w[36] = __int_as_float(i0);
-            w[37] = __int_as_float(j0);
-            w[38] = __int_as_float(k0);
-            w[39] = __int_as_float((int)p);  // original position index
-            float4 *dst = reinterpret_cast<float4 *>(recs + (long long)(base[b] + rank) * REC);
-#pragma unroll
-            for (int e = 0; e < REC / 4; ++e) dst[e] = make_float4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+            unsigned char *dst = recs + (long long)(base[b] + rank) * RECB;
+            store_weights(dst, w);
+            *reinterpret_cast<int4 *>(dst + 36 * sizeof(T)) = make_int4(i0, j0, k0, (int)p);
         }
         __syncthreads();
     }
 }
 
 // -------------------------------------------------------------- kernel --
-// Launch shapes: warps per CTA, ring stages per warp, positions per item.
-template <int WARPS_, int R_, int BP_>
-struct TCfg {
-    static constexpr int WARPS = WARPS_, R = R_, BP = BP_;
-};
-using CfgB = TCfg<12, 2, 8>;   // 12 warps, one slab in flight per warp while it computes one
-
 struct ItemInfo {
     long long b0;
     int nb, m, c, G, valid, pad;
@@ -330,19 +401,22 @@ struct GroupDesc {
     int x[PW], y[PW], z[PW];  // i0, j0, k0 (z = k0 is the fastest table dim after lanes)
     unsigned bytes;           // valid positions x slab bytes
     int c0, m;
-    bool any;
 };
 
-template <int KIND, int CW, class C>
+template <int KIND, typename T, int CW, class C>
 __global__ void __launch_bounds__(C::WARPS * 32, 1)
     eval_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Args a) {
     constexpr int WARPS = C::WARPS, BP = C::BP;
     static_assert(C::R == 2, "the issue path runs exactly one slab ahead");
     constexpr int R = 2;
     constexpr int S = NS<KIND>::S;
-    constexpr int PW = 128 / CW;       // positions per warp step
-    constexpr int LPP = CW / 4;        // lanes per position
-    constexpr int SLAB = CW * 16 * 4;  // bytes per (position, i) slab
+    constexpr int W = TT<T>::W;
+    constexpr int RECB = TT<T>::RECB;
+    constexpr int PW = 32 * W / CW;              // positions per warp step
+    constexpr int LPP = CW / W;                  // lanes per position
+    constexpr int SLAB = CW * 16 * sizeof(T);    // bytes per (position, i) slab
+    using AV = typename Acc<T>::V;
+    constexpr int AN = Acc<T>::N;
     static_assert(PW * SLAB == STAGE, "stage must hold one warp step");
     static_assert(BP % PW == 0, "items hold whole groups");
 
@@ -352,10 +426,9 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
     unsigned long long *bars =
         reinterpret_cast<unsigned long long *>(smem + (size_t)WARPS * R * STAGE) + warp * (R + 2);
     unsigned long long *rbar = bars + R;  // record barriers of slots 0/1
-    float *recs = reinterpret_cast<float *>(smem + (size_t)WARPS * R * STAGE + WARPS * (R + 2) * 8) +
-                  warp * 2 * BP * REC;
+    unsigned char *recs = smem + (size_t)WARPS * R * STAGE + WARPS * (R + 2) * 8 + (size_t)warp * 2 * BP * RECB;
     ItemInfo *info = reinterpret_cast<ItemInfo *>(smem + (size_t)WARPS * R * STAGE + WARPS * (R + 2) * 8 +
-                                                  WARPS * 2 * BP * REC * 4) + warp * 2;
+                                                  (size_t)WARPS * 2 * BP * RECB) + warp * 2;
 
     if (lane == 0) {
         for (int s = 0; s < R + 2; ++s) mbar_init(&bars[s], 1);
@@ -378,8 +451,8 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
                 it.nb = (int)min((long long)BP, a.n_pos - it.b0);
                 it.G = (it.nb + PW - 1) / PW;
                 if (a.proxy_fence) fence_proxy_async();  // WAR on the slot, see issue()
-                mbar_arrive_expect_tx(&rbar[slot], (unsigned)(it.nb * REC * 4));
-                bulk_load(recs + slot * BP * REC, a.recs + it.b0 * REC, (unsigned)(it.nb * REC * 4), &rbar[slot]);
+                mbar_arrive_expect_tx(&rbar[slot], (unsigned)(it.nb * RECB));
+                bulk_load(recs + slot * BP * RECB, a.recs + it.b0 * RECB, (unsigned)(it.nb * RECB), &rbar[slot]);
             } else {
                 it.b0 = 0;
                 it.nb = it.m = it.c = it.G = 0;
@@ -392,33 +465,33 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
     // lane 0: descriptor of group g of the item in `slot` (records must have landed)
     auto prepare = [&](GroupDesc<PW> &d, int slot, int g) {
         const ItemInfo it = info[slot];
-        const float *rc = recs + slot * BP * REC;
+        const unsigned char *rc = recs + slot * BP * RECB;
         d.bytes = 0;
         d.c0 = it.c * CW;
         d.m = it.m;
 #pragma unroll
         for (int q = 0; q < PW; ++q) {
             const int p = g * PW + q;
-            const int4 cell = *reinterpret_cast<const int4 *>(rc + min(p, it.nb - 1) * REC + 36);
+            const int4 cell = *reinterpret_cast<const int4 *>(rc + min(p, it.nb - 1) * RECB + 36 * sizeof(T));
             const bool ok = p < it.nb && cell.x >= 0;
             d.x[q] = ok ? cell.x : -1;
             d.y[q] = cell.y;
             d.z[q] = cell.z;
             d.bytes += ok ? SLAB : 0;
         }
-        d.any = true;
     };
     // lane 0: issue slab ii of the described group into stage st
     auto issue = [&](const GroupDesc<PW> &d, int ii, int st, unsigned long long policy) {
         unsigned char *dst = ring + st * STAGE;
         // WAR only (LDS reads of this stage, all consumed before the
-        // __syncwarp above, then the TMA write): no proxy fence needed, as in
-        // a consumer-release / producer-acquire TMA pipeline.
+        // __syncwarp before this call, then the TMA write): no proxy fence
+        // needed, as in a consumer-release / producer-acquire TMA pipeline.
         if (a.proxy_fence) fence_proxy_async();
         mbar_arrive_expect_tx(&bars[st], d.bytes);
 #pragma unroll
         for (int q = 0; q < PW; ++q)
-            if (d.x[q] >= 0) tma_load_5d(dst + q * SLAB, &tmap, &bars[st], d.c0, d.z[q], d.y[q], d.x[q] + ii, d.m, policy);
+            if (d.x[q] >= 0)
+                tma_load_5d(dst + q * SLAB, &tmap, &bars[st], d.c0, d.z[q], d.y[q], d.x[q] + ii, d.m, policy);
     };
 
     const unsigned long long policy = l2_policy(a.evict_last);
@@ -428,7 +501,6 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
     unsigned ph0 = 0, ph1 = 0;    // stage barrier parities
     unsigned rph0 = 0, rph1 = 0;  // record barrier parities
     GroupDesc<PW> d;
-    d.any = false;
 
     fill(0);
     fill(1);
@@ -444,24 +516,23 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
     int cslot = 0;
     while (true) {
         const ItemInfo it = info[cslot];
-        const float *rc = recs + cslot * BP * REC;
+        const unsigned char *rc = recs + cslot * BP * RECB;
         for (int g = 0; g < it.G; ++g) {
             const int p = g * PW + pp;
-            const float *w = rc + min(p, it.nb - 1) * REC;
-            float wx[12], wy[12], wz[12];
+            const T *w = reinterpret_cast<const T *>(rc + min(p, it.nb - 1) * RECB);
+            T wx[12], wy[12], wz[12];
 #pragma unroll
-            for (int e = 0; e < 12; e += 4) {
-                const float4 x4 = *reinterpret_cast<const float4 *>(w + e);
-                const float4 y4 = *reinterpret_cast<const float4 *>(w + 12 + e);
-                const float4 z4 = *reinterpret_cast<const float4 *>(w + 24 + e);
-                wx[e] = x4.x, wx[e + 1] = x4.y, wx[e + 2] = x4.z, wx[e + 3] = x4.w;
-                wy[e] = y4.x, wy[e + 1] = y4.y, wy[e + 2] = y4.z, wy[e + 3] = y4.w;
-                wz[e] = z4.x, wz[e + 1] = z4.y, wz[e + 2] = z4.z, wz[e + 3] = z4.w;
+            for (int e = 0; e < 12; ++e) {
+                wx[e] = w[e];
+                wy[e] = w[12 + e];
+                wz[e] = w[24 + e];
             }
-            const bool finite = __float_as_int(w[36]) >= 0;
-            float2 acc[S][2];
+            const int4 cell = *reinterpret_cast<const int4 *>(rc + min(p, it.nb - 1) * RECB + 36 * sizeof(T));
+            AV acc[S][AN];
 #pragma unroll
-            for (int s = 0; s < S; ++s) acc[s][0] = acc[s][1] = make_float2(0.0f, 0.0f);
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int h = 0; h < AN; ++h) zero(acc[s][h]);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 // ---- issue the next step into the other stage (its previous
@@ -496,20 +567,16 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
                     mbar_wait(&bars[0], ph0);
                     ph0 ^= 1;
                 }
-                const float *slab = reinterpret_cast<const float *>(ring + st * STAGE + pp * SLAB) + vl * 4;
-                slab_fma2<KIND, CW>(slab, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
+                const T *slab = reinterpret_cast<const T *>(ring + st * STAGE + pp * SLAB) + vl * W;
+                slab_contract<KIND, CW>(slab, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
                 st ^= 1;
             }
             if (p < it.nb) {
-                const long long gp = __float_as_int(rc[p * REC + 39]);  // original index
+                const long long gp = cell.w;  // original index
                 const long long op = a.out_index ? a.out_index[gp] : gp;
-                float *o = a.out + op * a.out_pos_stride + (long long)it.m * a.nb + it.c * CW + vl * 4;
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    const float4 v = finite ? make_float4(acc[s][0].x, acc[s][0].y, acc[s][1].x, acc[s][1].y)
-                                            : make_float4(NAN, NAN, NAN, NAN);
-                    __stcs(reinterpret_cast<float4 *>(o + s * a.out_stream_stride), v);
-                }
+                T *o = reinterpret_cast<T *>(a.out) + op * a.out_pos_stride + (long long)it.m * a.nb + it.c * CW +
+                       vl * W;
+                store_lane<S>(o, a.out_stream_stride, acc, cell.x >= 0);
             }
         }
         __syncwarp();
@@ -539,95 +606,121 @@ static EncodeTiled get_encode() {
     return fn;
 }
 
-template <class C>
+template <typename T>
 constexpr size_t smem_bytes() {
-    return (size_t)C::WARPS * C::R * STAGE + C::WARPS * (C::R + 2) * 8 + C::WARPS * 2 * C::BP * REC * 4 +
+    using C = typename TT<T>::Cfg;
+    return (size_t)C::WARPS * C::R * STAGE + C::WARPS * (C::R + 2) * 8 + (size_t)C::WARPS * 2 * C::BP * TT<T>::RECB +
            C::WARPS * 2 * sizeof(ItemInfo);
 }
-static_assert(smem_bytes<CfgB>() <= 232448, "shared memory budget");
+static_assert(smem_bytes<float>() <= 232448, "shared memory budget");
+static_assert(smem_bytes<double>() <= 232448, "shared memory budget");
 
-template <int KIND, int CW, class C>
+template <int KIND, typename T, int CW>
 static int launch_t(const CUtensorMap &map, const Args &a, int sms, cudaStream_t st) {
-    constexpr size_t sm = smem_bytes<C>();
+    using C = typename TT<T>::Cfg;
+    constexpr size_t sm = smem_bytes<T>();
     const long long warps_needed = (a.n_items + 1) / 2;
     int grid = (int)min((long long)sms, (warps_needed + C::WARPS - 1) / C::WARPS);
     if (grid < 1) grid = 1;
-    cudaFuncSetAttribute(eval_tma_kernel<KIND, CW, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    eval_tma_kernel<KIND, CW, C><<<grid, C::WARPS * 32, sm, st>>>(map, a);
+    cudaFuncSetAttribute(eval_tma_kernel<KIND, T, CW, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    eval_tma_kernel<KIND, T, CW, C><<<grid, C::WARPS * 32, sm, st>>>(map, a);
     return check_launch("spo_eval (tma) launch");
 }
 
-template <int KIND, class C>
-static int launch_cw(int cw, const CUtensorMap &map, const Args &a, int sms, cudaStream_t st) {
-    switch (cw) {
-        case 32: return launch_t<KIND, 32, C>(map, a, sms, st);
-        case 64: return launch_t<KIND, 64, C>(map, a, sms, st);
-        default: return launch_t<KIND, 128, C>(map, a, sms, st);
+// chunk widths in elements: 128 / 256 / 512-byte rows
+template <int KIND, typename T>
+static int launch_cw(int cw_bytes, const CUtensorMap &map, const Args &a, int sms, cudaStream_t st) {
+    constexpr int E = (int)sizeof(T);
+    switch (cw_bytes) {
+        case 128: return launch_t<KIND, T, 128 / E>(map, a, sms, st);
+        case 256: return launch_t<KIND, T, 256 / E>(map, a, sms, st);
+        default: return launch_t<KIND, T, 512 / E>(map, a, sms, st);
     }
 }
 
+template <typename T>
+static int launch_kind(int kind, int cw_bytes, const CUtensorMap &map, const Args &a, int sms, cudaStream_t st) {
+    if (kind == SPO_KIND_V) return launch_cw<SPO_KIND_V, T>(cw_bytes, map, a, sms, st);
+    if (kind == SPO_KIND_VGL) return launch_cw<SPO_KIND_VGL, T>(cw_bytes, map, a, sms, st);
+    return launch_cw<SPO_KIND_VGH, T>(cw_bytes, map, a, sms, st);
+}
 
+static int rec_bytes(int dtype) { return dtype == SPO_F64 ? TT<double>::RECB : TT<float>::RECB; }
+static int item_positions(int dtype) { return dtype == SPO_F64 ? TT<double>::Cfg::BP : TT<float>::Cfg::BP; }
 
 }  // namespace tma
 
 // workspace: [header: ticket | bucket counts | bucket cursors] [bucket id per
 // position, 16-byte padded] [records, bucket-sorted]
-long long eval_tma_workspace_bytes(long long n_pos) {
-    return tma::WS_HEADER + ((n_pos + 15) / 16) * 16 + n_pos * tma::REC * 4;
+long long eval_tma_workspace_bytes(int dtype, long long n_pos) {
+    return tma::WS_HEADER + ((n_pos + 15) / 16) * 16 + n_pos * (long long)tma::rec_bytes(dtype);
 }
 
-
-// Called by spo_eval for fp32 FAST requests with a workspace.  Returns -1
-// when the TMA path cannot be used (the caller then uses the generic kernel).
-int eval_tma(int kind, const float *table, const TableGeom &geo, const GridArgs &g, const double *pos,
-             long long n_pos, float *out, long long ops, long long oss, const long long *out_index, int *status,
+// Called by spo_eval for FAST requests with a workspace.  Returns -1 when the
+// TMA path cannot be used (the caller then uses the generic kernel).
+// cw_request: chunk width in elements (0 = automatic).
+int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const GridArgs &g, const double *pos,
+             long long n_pos, void *out, long long ops, long long oss, const long long *out_index, int *status,
              void *workspace, long long ws_bytes, cudaStream_t st, int cw_request) {
     using namespace tma;
-    if (!workspace || ws_bytes < eval_tma_workspace_bytes(n_pos) || !aligned16(workspace)) return -1;
+    if (!workspace || ws_bytes < eval_tma_workspace_bytes(dtype, n_pos) || !aligned16(workspace)) return -1;
+    if (n_pos >= (1LL << 31)) return -1;  // records carry 32-bit original indices
     EncodeTiled encode = get_encode();
     if (!encode) return -1;
-    // chunk width: working set rows x CW x 4 B <= ~40 MB unless overridden (one
-    // die's share of L2, with room for the next unit and the output stream)
+    const int E = dtype == SPO_F64 ? 8 : 4;
+    // chunk width (bytes per row segment): one spatial block's rows x CW within
+    // ~40 MB (a die's share of L2 with room for the next unit and the output
+    // stream) -> 512 B for any realistic grid.
     const long long rows = (long long)geo.nxp * geo.nyp * geo.nzp;
-    int cw = cw_request;
-    if (cw == 0) {
-        cw = 32;
-        if (rows * 128 * 4 / NBUCKET <= (40LL << 20)) cw = 128;
-        else if (rows * 64 * 4 / NBUCKET <= (40LL << 20)) cw = 64;
+    int cwb = cw_request * E;
+    if (cwb == 0) {
+        cwb = 128;
+        if (rows * 512 / NBUCKET <= (40LL << 20)) cwb = 512;
+        else if (rows * 256 / NBUCKET <= (40LL << 20)) cwb = 256;
     }
-    while (cw > 32 && geo.nb % cw) cw >>= 1;
-    if (cw < 32 || geo.nb % cw) return -1;
+    while (cwb > 128 && (geo.nb * E) % cwb) cwb >>= 1;
+    if (cwb != 128 && cwb != 256 && cwb != 512) return -1;
+    if ((geo.nb * E) % cwb) return -1;
+    const int cw = cwb / E;
 
     CUtensorMap map;
     cuuint64_t dims[5] = {(cuuint64_t)geo.nb, (cuuint64_t)geo.nzp, (cuuint64_t)geo.nyp, (cuuint64_t)geo.nxp,
                           (cuuint64_t)geo.n_tiles};
-    cuuint64_t strides[4] = {(cuuint64_t)geo.nb * 4, (cuuint64_t)geo.nzp * geo.nb * 4,
-                             (cuuint64_t)geo.nyp * geo.nzp * geo.nb * 4, (cuuint64_t)geo.tile_stride * 4};
+    cuuint64_t strides[4] = {(cuuint64_t)geo.nb * E, (cuuint64_t)geo.nzp * geo.nb * E,
+                             (cuuint64_t)geo.nyp * geo.nzp * geo.nb * E, (cuuint64_t)geo.tile_stride * E};
     cuuint32_t box[5] = {(cuuint32_t)cw, 4, 4, 1, 1};
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float *>(table), dims, strides, box,
-                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = encode(&map, dtype == SPO_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        5, const_cast<void *>(table), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    {
+        const long long nbatch = (n_pos + item_positions(dtype) - 1) / item_positions(dtype);
+        if (nbatch * (long long)geo.n_tiles * (geo.nb / cw) >= (1LL << 32)) return -1;  // 32-bit tickets
+    }
 
-    if (n_pos >= (1LL << 31)) return -1;  // records carry 32-bit original indices
     unsigned char *ws = static_cast<unsigned char *>(workspace);
     unsigned *counts = reinterpret_cast<unsigned *>(ws + 256);
     unsigned *cursors = reinterpret_cast<unsigned *>(ws + 512);
     unsigned char *bucket = ws + WS_HEADER;
-    float *recs = reinterpret_cast<float *>(ws + WS_HEADER + ((n_pos + 15) / 16) * 16);
+    unsigned char *recs = ws + WS_HEADER + ((n_pos + 15) / 16) * 16;
     if (cudaMemsetAsync(ws, 0, WS_HEADER, st) != cudaSuccess) return check_launch("workspace reset");
     {
         long long blocks = (n_pos + 255) / 256;
         if (blocks > 148LL * 16) blocks = 148LL * 16;
         bucket_count_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, bucket, counts);
-        prologue_records_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, bucket, counts, cursors, recs,
-                                                                  status);
+        if (dtype == SPO_F64)
+            prologue_records_kernel<double>
+                <<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, bucket, counts, cursors, recs, status);
+        else
+            prologue_records_kernel<float>
+                <<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, bucket, counts, cursors, recs, status);
         int rc = check_launch("spo_eval (prologue) launch");
         if (rc) return rc;
     }
 
-    const int BP = CfgB::BP;
+    const int BP = item_positions(dtype);
     Args a;
     a.recs = recs;
     a.ticket = reinterpret_cast<unsigned *>(ws);
@@ -644,14 +737,12 @@ int eval_tma(int kind, const float *table, const TableGeom &geo, const GridArgs 
     a.evict_last = !(env_hint && env_hint[0] == '0');
     static const char *env_fence = getenv("SPO_PROXY_FENCE");
     a.proxy_fence = env_fence && env_fence[0] == '1';
-    if (a.n_items >= (1LL << 32)) return -1;  // 32-bit ticket counter
 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (kind == SPO_KIND_V) return launch_cw<SPO_KIND_V, CfgB>(cw, map, a, sms, st);
-    if (kind == SPO_KIND_VGL) return launch_cw<SPO_KIND_VGL, CfgB>(cw, map, a, sms, st);
-    return launch_cw<SPO_KIND_VGH, CfgB>(cw, map, a, sms, st);
+    if (dtype == SPO_F64) return launch_kind<double>(kind, cwb, map, a, sms, st);
+    return launch_kind<float>(kind, cwb, map, a, sms, st);
 }
 
 }  // namespace spo

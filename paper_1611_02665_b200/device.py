@@ -47,19 +47,19 @@ SPATIAL_BUCKETS = 64  # csrc/spo_eval_tma.cu NBUCKET (4 x 4 x 4 blocks)
 
 
 def auto_tile_size(grid: GridSpec, n_splines: int, dtype=np.float32):
-    """AoSoA tile width (splines) so that one tile slice -- (n+3)^3 rows x tile
-    lanes -- fits the L2 working-set target: 128, 64 or 32 lanes (the TMA
-    kernel's chunk widths); untiled when N fits in one such tile.  Tiles are
+    """AoSoA tile width (splines): the widest of 512/256/128-byte rows (the
+    TMA kernel's chunk widths) whose per-spatial-block slice fits the L2
+    working-set target; untiled when N fits in one such tile.  Tiles are
     multiples of the 128-byte lane quantum, so spline n keeps output lane n."""
     rows = int(np.prod(grid.padded_counts))
     item = np.dtype(dtype).itemsize
     q = lane_quantum(dtype)
     tile = q
-    # fp32 goes through the TMA kernel, which also bins positions into
-    # SPATIAL_BUCKETS blocks of the grid: its working set is a block's rows
-    buckets = SPATIAL_BUCKETS if np.dtype(dtype) == np.float32 else 1
-    for cand in (128, 64, 32):
-        if cand % q == 0 and rows * cand * item // buckets <= TILE_SLICE_BYTES:
+    # the TMA kernel bins positions into SPATIAL_BUCKETS blocks of the grid:
+    # its working set is one block's rows x tile (512, 256 or 128-byte rows)
+    for row_bytes in (512, 256, 128):
+        cand = row_bytes // item
+        if cand % q == 0 and rows * row_bytes // SPATIAL_BUCKETS <= TILE_SLICE_BYTES:
             tile = cand
             break
     if n_splines <= tile:

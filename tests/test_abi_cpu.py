@@ -36,7 +36,8 @@ def test_library_exports_every_header_symbol(lib):
 def test_abi_version(lib):
     assert lib.spo_abi_version() == 2
     assert lib.spo_eval_workspace_bytes(2, 0, 0, 1000) >= 1000 * 160
-    assert lib.spo_eval_workspace_bytes(2, 1, 0, 1000) == 0
+    assert lib.spo_eval_workspace_bytes(2, 1, 0, 1000) >= 1000 * 304  # fp64 records
+    assert lib.spo_eval_workspace_bytes(2, 0, 1, 1000) == 0  # strict: generic kernel only
     assert lib.spo_eval_workspace_bytes(9, 0, 0, 1000) == -1
 
 

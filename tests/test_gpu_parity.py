@@ -249,6 +249,9 @@ def test_fp64_within_1e12(torch, kind):
     assert ok, worst
     tiled = DeviceTable.normal_f64(grid, 40, seed=3, tile_size=16)
     np.testing.assert_array_equal(run(tiled, kind, pos), got)
+    # the fp64 TMA-pipelined kernel runs the generic kernel's DFMA sequence
+    for table in (dt, tiled, DeviceTable.normal_f64(grid, 40, seed=3, tile_size=32)):
+        np.testing.assert_array_equal(run(table, kind, pos, pipeline=True), got)
 
 
 def test_fp64_normal_fill_moments(torch):
