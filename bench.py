@@ -58,7 +58,6 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sort-host", action="store_true", help="experiment: pre-sorted positions")
     return ap.parse_args()
 
 
@@ -266,26 +265,11 @@ def run_b200(args):
     bounds = [(lo, min(P, lo + chunk)) for lo in range(0, P, chunk)]
     stream = torch.cuda.current_stream(dev)
 
-    oidx = None
-    if args.sort_host:  # EXPERIMENT: chunk-local cell sort on the host (not timed)
-        n = cfg.grid.nx
-        cell = np.floor(np.mod(pos_np, 1.0) * n).astype(np.int64).clip(0, n - 1)
-        key = (cell[:, 0] * n + cell[:, 1]) * n + cell[:, 2]
-        sp = np.empty_like(pos_np)
-        oi = np.empty(P, dtype=np.int64)
-        for lo, hi in bounds:
-            perm = np.argsort(key[lo:hi], kind="stable")
-            sp[lo:hi] = pos_np[lo + perm]
-            oi[lo:hi] = perm
-        pos = torch.from_numpy(sp).to(dev)
-        oidx = torch.from_numpy(oi).to(dev)
-
     def step(events=None):
         for b, (lo, hi) in enumerate(bounds):
             if events is not None:
                 events[b][0].record(stream)
-            evaluate(table, kind, pos[lo:hi], out, mode=args.mode, check=False,
-                     out_index=None if oidx is None else oidx[lo:hi])
+            evaluate(table, kind, pos[lo:hi], out, mode=args.mode, check=False)
             if events is not None:
                 events[b][1].record(stream)
 

@@ -54,6 +54,22 @@ inline int bind_device(const void *ptr) {
     return SPO_OK;
 }
 
+// Every device buffer of a call must live on the device bind_device picked:
+// a foreign pointer would fault inside the kernel, so reject it up front.
+inline int check_on_device(const void *ptr, const char *what) {
+    if (!ptr) return SPO_OK;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SPO_ERR_CONTRACT, "%s (%p) is not a CUDA allocation", what, ptr);
+    }
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if ((at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) || at.device != cur)
+        return fail(SPO_ERR_CONTRACT, "%s (%p) is not memory of device %d", what, ptr, cur);
+    return SPO_OK;
+}
+
 inline int check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SPO_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));

@@ -343,6 +343,10 @@ extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const 
 
     rc = bind_device(out);
     if (rc) return rc;
+    if ((rc = check_on_device(table, "table")) || (rc = check_on_device(pos, "positions")) ||
+        (rc = check_on_device(out_index, "out_index")) || (rc = check_on_device(status, "status")) ||
+        (rc = check_on_device(workspace, "workspace")))
+        return rc;
     if (mode == SPO_MODE_FAST) {
         static const char *env_tma = getenv("SPO_TMA");
         static const char *env_cw = getenv("SPO_CW");

@@ -235,6 +235,8 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
         raise ContractError(f"unknown mode {mode!r}")
     if mode == "strict" and dt.dtype != np.float32:
         raise ContractError("strict mode reproduces the fp32 reference kernels only")
+    if status is not None and (status.device != device or status.dtype != torch.int32 or status.numel() < 1):
+        raise ContractError("status must be an int32 CUDA tensor on the table device")
     own_status = status is None and check
     if own_status:
         status = torch.zeros(1, dtype=torch.int32, device=device)
