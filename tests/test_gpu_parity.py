@@ -302,3 +302,25 @@ def test_pipelined_edge_cases(torch, golden_mapping):
     torch.cuda.synchronize()
     assert torch.equal(a, base)
     assert torch.equal(b[:, :4], base[:, :4])
+
+
+def test_abi_rejects_host_pointers(torch, cfg1):
+    """A host pointer where device memory is expected is a ContractError, not
+    a kernel fault."""
+    import ctypes
+
+    _, dt = cfg1
+    L = _abi.load()
+    pos = torch.zeros((4, 3), dtype=torch.float64, device="cuda")
+    out = torch.empty((4, 1, dt.lanes), dtype=torch.float32, device="cuda")
+    host_table = np.zeros(dt.data.numel(), dtype=np.float32)
+    g = dt.grid
+    rc = L.spo_eval(0, 0, 0, host_table.ctypes.data, _abi.i32x3(g.counts), dt.nb, dt.n_tiles,
+                    _abi.f64x3(g.inverse_spacings), _abi.f64x3(g.spacings), pos.data_ptr(), 4,
+                    out.data_ptr(), dt.lanes, dt.lanes, None, None, None, 0, ctypes.c_void_p(0))
+    assert rc == 1 and b"table" in L.spo_last_error()
+    host_pos = np.zeros((4, 3))
+    rc = L.spo_eval(0, 0, 0, dt.data.data_ptr(), _abi.i32x3(g.counts), dt.nb, dt.n_tiles,
+                    _abi.f64x3(g.inverse_spacings), _abi.f64x3(g.spacings), host_pos.ctypes.data, 4,
+                    out.data_ptr(), dt.lanes, dt.lanes, None, None, None, 0, ctypes.c_void_p(0))
+    assert rc == 1 and b"positions" in L.spo_last_error()
