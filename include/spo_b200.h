@@ -60,7 +60,7 @@
 extern "C" {
 #endif
 
-#define SPO_ABI_VERSION 2
+#define SPO_ABI_VERSION 3
 
 /* kernel kinds: KernelKind (kernels.py:26-51) */
 #define SPO_KIND_V 0
@@ -109,6 +109,23 @@ int spo_eval(int kind, int dtype, int mode, const void *table, const int32_t *n3
 
 /* Workspace spo_eval wants for this request (0 = none used, -1 = bad args). */
 int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64_t n_pos);
+
+/*
+ * Fused consumer epilogue (beyond the reference): the
+ * determinant-ratio style contraction of every output stream with a
+ * per-position coefficient row, without writing the [P][S][lanes] outputs:
+ *   ratios[p][s] = sum_n stream_s(p, n) * coef[p * coef_stride + lane(n)]
+ * accumulated in fp64 (per-chunk partials reduced in a fixed order:
+ * deterministic).  coef (device, table dtype) is in output-lane layout with
+ * zeros in padding lanes; ratios (device) is [n_pos][S] float64.  Needs
+ * spo_eval_ratios_workspace_bytes() of workspace; rows must be multiples of
+ * 512 bytes (tiles of 128 fp32 / 64 fp64 lanes, or untiled N padded so).
+ */
+int64_t spo_eval_ratios_workspace_bytes(int kind, int dtype, int32_t nb, int32_t n_tiles, int64_t n_pos);
+int spo_eval_ratios(int kind, int dtype, const void *table, const int32_t *n3, int32_t nb, int32_t n_tiles,
+                    const double *dinv3, const double *delta3, const double *pos, int64_t n_pos,
+                    const void *coef, int64_t coef_stride, double *ratios, int32_t *status,
+                    void *workspace, int64_t workspace_bytes, void *stream);
 
 /*
  * Per-position prologue: idx [n_pos][3] int32 (i0, j0, k0), t [n_pos][3]

@@ -47,7 +47,7 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    tmp = LIB + ".tmp"
+    tmp = f"{LIB}.{os.getpid()}.tmp"  # concurrent builders never share a temp file
     cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-o", tmp, *SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(PKG, "csrc", "build.log")

@@ -292,8 +292,10 @@ static int launch(const EvalArgs &a, dim3 grid, dim3 block, size_t smem, cudaStr
 namespace spo {
 int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const GridArgs &g, const double *pos,
              long long n_pos, void *out, long long ops, long long oss, const long long *out_index, int *status,
-             void *workspace, long long ws_bytes, cudaStream_t st, int cw_request);
+             void *workspace, long long ws_bytes, cudaStream_t st, int cw_request, const void *coef = nullptr,
+             long long coef_stride = 0, double *ratios = nullptr);
 long long eval_tma_workspace_bytes(int dtype, long long n_pos);
+long long eval_tma_ratio_bytes(int kind, int dtype, long long nb, long long n_tiles, long long n_pos);
 }
 
 using namespace spo;
@@ -429,4 +431,55 @@ extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const 
         case SPO_KIND_VGL: return launch<SPO_KIND_VGL, float, false>(a, grid, block, smem, st);
         default: return launch<SPO_KIND_VGH, float, false>(a, grid, block, smem, st);
     }
+}
+
+// ------------------------------------------------------------ ratios ----
+extern "C" int64_t spo_eval_ratios_workspace_bytes(int kind, int dtype, int32_t nb, int32_t n_tiles,
+                                                   int64_t n_pos) {
+    if (kind < SPO_KIND_V || kind > SPO_KIND_VGH || n_pos < 0 || nb <= 0 || n_tiles <= 0) return -1;
+    if (dtype != SPO_F32 && dtype != SPO_F64) return -1;
+    const long long extra = eval_tma_ratio_bytes(kind, dtype, nb, n_tiles, n_pos);
+    if (extra < 0) return -1;
+    return eval_tma_workspace_bytes(dtype, n_pos) + extra;
+}
+
+extern "C" int spo_eval_ratios(int kind, int dtype, const void *table, const int32_t *n3, int32_t nb,
+                               int32_t n_tiles, const double *dinv3, const double *delta3, const double *pos,
+                               int64_t n_pos, const void *coef, int64_t coef_stride, double *ratios,
+                               int32_t *status, void *workspace, int64_t workspace_bytes, void *stream) {
+    if (kind < SPO_KIND_V || kind > SPO_KIND_VGH) return fail(SPO_ERR_CONTRACT, "unknown kind %d", kind);
+    if (dtype != SPO_F32 && dtype != SPO_F64) return fail(SPO_ERR_CONTRACT, "unknown dtype %d", dtype);
+    TableGeom geo;
+    int rc = make_geom(n3, nb, n_tiles, dtype, &geo);
+    if (rc) return rc;
+    if (n_pos < 0) return fail(SPO_ERR_CONTRACT, "n_pos=%lld < 0", (long long)n_pos);
+    if (n_pos == 0) return ok();
+    if (!table || !pos || !coef || !ratios || !dinv3 || !delta3 || !workspace)
+        return fail(SPO_ERR_CONTRACT, "NULL pointer argument");
+    const int W = dtype == SPO_F64 ? 2 : 4;
+    if (!aligned16(table) || !aligned16(coef) || coef_stride % W)
+        return fail(SPO_ERR_CONTRACT, "table/coef must be 16-byte aligned, coef_stride a multiple of %d", W);
+    if (coef_stride < (long long)nb * n_tiles)
+        return fail(SPO_ERR_CONTRACT, "coef_stride %lld shorter than the %lld table lanes", (long long)coef_stride,
+                    (long long)nb * n_tiles);
+    for (int ax = 0; ax < 3; ++ax)
+        if (!(dinv3[ax] > 0.0) || !(delta3[ax] > 0.0))
+            return fail(SPO_ERR_CONFIG, "grid spacing on axis %d must be positive", ax);
+    rc = bind_device(ratios);
+    if (rc) return rc;
+    if ((rc = check_on_device(table, "table")) || (rc = check_on_device(pos, "positions")) ||
+        (rc = check_on_device(coef, "coef")) || (rc = check_on_device(status, "status")) ||
+        (rc = check_on_device(workspace, "workspace")))
+        return rc;
+    GridArgs g;
+    for (int ax = 0; ax < 3; ++ax) {
+        g.dinv[ax] = dinv3[ax];
+        g.cnt[ax] = (double)n3[ax];
+        g.delta[ax] = delta3[ax];
+        g.n[ax] = n3[ax];
+    }
+    rc = eval_tma(kind, dtype, table, geo, g, pos, n_pos, nullptr, 0, 0, nullptr, status, workspace,
+                  workspace_bytes, reinterpret_cast<cudaStream_t>(stream), 0, coef, coef_stride, ratios);
+    if (rc < 0) return fail(SPO_ERR_CONFIG, "the fused ratio epilogue is unavailable for this request");
+    return rc;
 }

@@ -73,6 +73,11 @@ struct Args {
     const long long *out_index;
     int evict_last;             // L2 evict_last hint on table slabs
     int proxy_fence;            // fence.proxy.async before reusing a stage (diagnostic)
+    // fused ratio epilogue (RATIO kernels): per (unit, position) partial dot
+    // products of every stream with the caller's coefficient row
+    const void *coef;           // [n_pos][coef_stride] in output-lane layout, pad lanes 0
+    long long coef_stride;
+    double *partials;           // [units][n_pos][S]
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -403,7 +408,43 @@ struct GroupDesc {
     int c0, m;
 };
 
-template <int KIND, typename T, int CW, class C>
+// Fused epilogue: this lane's orbitals dotted with its coefficient entries in
+// fp64, reduced over the LPP lanes of the position (xor shuffles stay inside
+// the lane segment), written once per (unit, position) by the segment leader.
+// fp32 tables: the lane's 4-term dot and the lane-segment reduction run in
+// fp32 (one chunk = at most 128 orbitals); chunks are summed in fp64.
+template <int S, int LPP>
+__device__ __forceinline__ void ratio_partials(const float2 (&acc)[S][2], const float *coef, bool live,
+                                               double (&part)[S]) {
+    float4 cf = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) cf = __ldg(reinterpret_cast<const float4 *>(coef));
+    float f[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+        f[s] = live ? __fmaf_rn(acc[s][1].y, cf.w,
+                                __fmaf_rn(acc[s][1].x, cf.z, __fmaf_rn(acc[s][0].y, cf.y, acc[s][0].x * cf.x)))
+                    : 0.0f;
+#pragma unroll
+    for (int off = LPP / 2; off > 0; off >>= 1)
+#pragma unroll
+        for (int s = 0; s < S; ++s) f[s] += __shfl_xor_sync(0xffffffffu, f[s], off);
+#pragma unroll
+    for (int s = 0; s < S; ++s) part[s] = f[s];
+}
+template <int S, int LPP>
+__device__ __forceinline__ void ratio_partials(const double2 (&acc)[S][1], const double *coef, bool live,
+                                               double (&part)[S]) {
+    double2 cf = make_double2(0.0, 0.0);
+    if (live) cf = __ldg(reinterpret_cast<const double2 *>(coef));
+#pragma unroll
+    for (int s = 0; s < S; ++s) part[s] = live ? __fma_rn(acc[s][0].y, cf.y, acc[s][0].x * cf.x) : 0.0;
+#pragma unroll
+    for (int off = LPP / 2; off > 0; off >>= 1)
+#pragma unroll
+        for (int s = 0; s < S; ++s) part[s] += __shfl_xor_sync(0xffffffffu, part[s], off);
+}
+
+template <int KIND, typename T, int CW, class C, bool RATIO>
 __global__ void __launch_bounds__(C::WARPS * 32, 1)
     eval_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Args a) {
     constexpr int WARPS = C::WARPS, BP = C::BP;
@@ -571,7 +612,20 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
                 slab_contract<KIND, CW>(slab, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
                 st ^= 1;
             }
-            if (p < it.nb) {
+            if constexpr (RATIO) {
+                const bool live = p < it.nb;
+                const long long gp = live ? cell.w : 0;
+                const T *cf = reinterpret_cast<const T *>(a.coef) + gp * a.coef_stride + (long long)it.m * a.nb +
+                              it.c * CW + vl * W;
+                double part[S];
+                ratio_partials<S, LPP>(acc, cf, live, part);  // reduced over the position's lanes
+                if (live && vl == 0) {
+                    const long long u = (long long)it.m * a.chunks + it.c;
+                    double *dst = a.partials + (u * a.n_pos + gp) * S;
+#pragma unroll
+                    for (int s = 0; s < S; ++s) dst[s] = cell.x >= 0 ? part[s] : (double)NAN;
+                }
+            } else if (p < it.nb) {
                 const long long gp = cell.w;  // original index
                 const long long op = a.out_index ? a.out_index[gp] : gp;
                 T *o = reinterpret_cast<T *>(a.out) + op * a.out_pos_stride + (long long)it.m * a.nb + it.c * CW +
@@ -615,34 +669,49 @@ constexpr size_t smem_bytes() {
 static_assert(smem_bytes<float>() <= 232448, "shared memory budget");
 static_assert(smem_bytes<double>() <= 232448, "shared memory budget");
 
-template <int KIND, typename T, int CW>
+template <int KIND, typename T, int CW, bool RATIO>
 static int launch_t(const CUtensorMap &map, const Args &a, int sms, cudaStream_t st) {
     using C = typename TT<T>::Cfg;
     constexpr size_t sm = smem_bytes<T>();
     const long long warps_needed = (a.n_items + 1) / 2;
     int grid = (int)min((long long)sms, (warps_needed + C::WARPS - 1) / C::WARPS);
     if (grid < 1) grid = 1;
-    cudaFuncSetAttribute(eval_tma_kernel<KIND, T, CW, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    eval_tma_kernel<KIND, T, CW, C><<<grid, C::WARPS * 32, sm, st>>>(map, a);
+    cudaFuncSetAttribute(eval_tma_kernel<KIND, T, CW, C, RATIO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    eval_tma_kernel<KIND, T, CW, C, RATIO><<<grid, C::WARPS * 32, sm, st>>>(map, a);
     return check_launch("spo_eval (tma) launch");
 }
 
-// chunk widths in elements: 128 / 256 / 512-byte rows
+// chunk widths in elements: 128 / 256 / 512-byte rows (the fused ratio
+// epilogue is instantiated for the 512-byte chunks only)
 template <int KIND, typename T>
-static int launch_cw(int cw_bytes, const CUtensorMap &map, const Args &a, int sms, cudaStream_t st) {
+static int launch_cw(int cw_bytes, bool ratio, const CUtensorMap &map, const Args &a, int sms, cudaStream_t st) {
     constexpr int E = (int)sizeof(T);
+    if (ratio) return launch_t<KIND, T, 512 / E, true>(map, a, sms, st);
     switch (cw_bytes) {
-        case 128: return launch_t<KIND, T, 128 / E>(map, a, sms, st);
-        case 256: return launch_t<KIND, T, 256 / E>(map, a, sms, st);
-        default: return launch_t<KIND, T, 512 / E>(map, a, sms, st);
+        case 128: return launch_t<KIND, T, 128 / E, false>(map, a, sms, st);
+        case 256: return launch_t<KIND, T, 256 / E, false>(map, a, sms, st);
+        default: return launch_t<KIND, T, 512 / E, false>(map, a, sms, st);
     }
 }
 
 template <typename T>
-static int launch_kind(int kind, int cw_bytes, const CUtensorMap &map, const Args &a, int sms, cudaStream_t st) {
-    if (kind == SPO_KIND_V) return launch_cw<SPO_KIND_V, T>(cw_bytes, map, a, sms, st);
-    if (kind == SPO_KIND_VGL) return launch_cw<SPO_KIND_VGL, T>(cw_bytes, map, a, sms, st);
-    return launch_cw<SPO_KIND_VGH, T>(cw_bytes, map, a, sms, st);
+static int launch_kind(int kind, int cw_bytes, bool ratio, const CUtensorMap &map, const Args &a, int sms,
+                       cudaStream_t st) {
+    if (kind == SPO_KIND_V) return launch_cw<SPO_KIND_V, T>(cw_bytes, ratio, map, a, sms, st);
+    if (kind == SPO_KIND_VGL) return launch_cw<SPO_KIND_VGL, T>(cw_bytes, ratio, map, a, sms, st);
+    return launch_cw<SPO_KIND_VGH, T>(cw_bytes, ratio, map, a, sms, st);
+}
+
+// ratios[p][s] = sum over units u (in order) of partials[u][p][s]: deterministic.
+__global__ void ratio_reduce_kernel(const double *__restrict__ partials, long long units, long long n,
+                                    double *__restrict__ ratios) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (long long u = 0; u < units; ++u) s += partials[u * n + e];
+        ratios[e] = s;
+    }
 }
 
 static int rec_bytes(int dtype) { return dtype == SPO_F64 ? TT<double>::RECB : TT<float>::RECB; }
@@ -656,17 +725,35 @@ long long eval_tma_workspace_bytes(int dtype, long long n_pos) {
     return tma::WS_HEADER + ((n_pos + 15) / 16) * 16 + n_pos * (long long)tma::rec_bytes(dtype);
 }
 
+// Extra workspace of the fused ratio epilogue: fp64 partials [units][n_pos][S]
+// with units = n_tiles x (row bytes / 512); -1 when the row is not a multiple
+// of 512 bytes (the epilogue runs with 512-byte chunks only).
+long long eval_tma_ratio_bytes(int kind, int dtype, long long nb, long long n_tiles, long long n_pos) {
+    const long long row = nb * (dtype == SPO_F64 ? 8 : 4);
+    if (row % 512) return -1;
+    const int S = kind == SPO_KIND_V ? 1 : (kind == SPO_KIND_VGL ? 5 : 10);
+    return n_tiles * (row / 512) * n_pos * S * 8;
+}
+
 // Called by spo_eval for FAST requests with a workspace.  Returns -1 when the
 // TMA path cannot be used (the caller then uses the generic kernel).
-// cw_request: chunk width in elements (0 = automatic).
+// cw_request: chunk width in elements (0 = automatic).  With `ratios` set the
+// fused epilogue replaces the output stores: ratios[p][s] = sum_n
+// stream_s(p, n) * coef[p][lane(n)] in fp64 (coef in output-lane layout).
 int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const GridArgs &g, const double *pos,
              long long n_pos, void *out, long long ops, long long oss, const long long *out_index, int *status,
-             void *workspace, long long ws_bytes, cudaStream_t st, int cw_request) {
+             void *workspace, long long ws_bytes, cudaStream_t st, int cw_request, const void *coef = nullptr,
+             long long coef_stride = 0, double *ratios = nullptr) {
     using namespace tma;
-    if (!workspace || ws_bytes < eval_tma_workspace_bytes(dtype, n_pos) || !aligned16(workspace)) return -1;
+    const bool ratio = ratios != nullptr;
+    const long long partial_bytes = ratio ? eval_tma_ratio_bytes(kind, dtype, geo.nb, geo.n_tiles, n_pos) : 0;
+    if (ratio && partial_bytes < 0) return fail(SPO_ERR_CONFIG, "ratio epilogue needs rows of 512-byte multiples");
+    if (!workspace || ws_bytes < eval_tma_workspace_bytes(dtype, n_pos) + partial_bytes || !aligned16(workspace))
+        return ratio ? fail(SPO_ERR_CONTRACT, "workspace too small for the ratio epilogue") : -1;
     if (n_pos >= (1LL << 31)) return -1;  // records carry 32-bit original indices
     EncodeTiled encode = get_encode();
-    if (!encode) return -1;
+    if (!encode) return ratio ? fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable") : -1;
+    if (ratio) cw_request = 512 / (dtype == SPO_F64 ? 8 : 4);
     const int E = dtype == SPO_F64 ? 8 : 4;
     // chunk width (bytes per row segment): one spatial block's rows x CW within
     // ~40 MB (a die's share of L2 with room for the next unit and the output
@@ -737,12 +824,21 @@ int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const
     a.evict_last = !(env_hint && env_hint[0] == '0');
     static const char *env_fence = getenv("SPO_PROXY_FENCE");
     a.proxy_fence = env_fence && env_fence[0] == '1';
+    a.coef = coef;
+    a.coef_stride = coef_stride;
+    a.partials = ratio ? reinterpret_cast<double *>(ws + eval_tma_workspace_bytes(dtype, n_pos)) : nullptr;
 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (dtype == SPO_F64) return launch_kind<double>(kind, cwb, map, a, sms, st);
-    return launch_kind<float>(kind, cwb, map, a, sms, st);
+    const int rc = dtype == SPO_F64 ? launch_kind<double>(kind, cwb, ratio, map, a, sms, st)
+                                    : launch_kind<float>(kind, cwb, ratio, map, a, sms, st);
+    if (rc || !ratio) return rc;
+    const int S = kind == SPO_KIND_V ? 1 : (kind == SPO_KIND_VGL ? 5 : 10);
+    const long long n = n_pos * S;
+    const long long blocks = min((n + 255) / 256, 148LL * 16);
+    ratio_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(a.partials, (long long)geo.n_tiles * a.chunks, n, ratios);
+    return check_launch("spo_eval_ratios (reduce) launch");
 }
 
 }  // namespace spo

@@ -27,7 +27,7 @@ import numpy as np
 from . import _abi
 from .coeffs import CoeffTableAoS, CoeffTableSoA, TiledCoeffTable, aligned_zeros, padded_count
 from .device import DeviceTable, _resolve_device, _stream_ptr, as_device_table
-from .errors import ContractError, DomainError
+from .errors import ConfigError, ContractError, DomainError
 
 
 class KernelKind(enum.Enum):
@@ -272,6 +272,56 @@ def evaluate_vgl(table, positions, out=None, **kw):
 
 def evaluate_vgh(table, positions, out=None, **kw):
     return evaluate(table, KernelKind.VGH, positions, out, **kw)
+
+
+def evaluate_ratios(table, kind, positions, coef, *, status=None, check: bool = True):
+    """Fused consumer epilogue: for every position p
+    and stream s, ratios[p, s] = sum_n stream_s(p, n) * coef[p, n], accumulated
+    in fp64, without materialising the [P][S][N] outputs -- in QMC, coef[p]
+    is the moved electron's column of the inverse Slater matrix and the
+    ratios are the determinant ratio and its gradient / Laplacian / Hessian
+    numerators.  coef: (P, N) of the table dtype (device or host).  Returns a
+    (P, S) float64 CUDA tensor.  Deterministic (fixed-order reduction)."""
+    torch = _torch()
+    kind = as_kind(kind)
+    dt = as_device_table(table)
+    device = dt.device
+    pos = _positions_tensor(positions, device)
+    P = pos.shape[0]
+    S = kind.output_streams_soa
+    tdt = torch.float64 if dt.dtype == np.float64 else torch.float32
+    coef = torch.as_tensor(coef, device=device)
+    if coef.dim() != 2 or coef.shape[0] != P or coef.shape[1] != dt.n_splines:
+        raise ContractError(f"coef must be (P={P}, N={dt.n_splines}), got {tuple(coef.shape)}")
+    if dt.lanes == dt.n_splines and dt.nb == dt.tile_size:  # lane(n) == n: use coef as is
+        lanes = coef.to(tdt).contiguous()
+    else:
+        lanes = torch.zeros((P, dt.lanes), dtype=tdt, device=device)  # output-lane layout, pad lanes 0
+        if dt.tiled:
+            lanes.index_copy_(1, dt.lane_index(), coef.to(tdt))
+        else:
+            lanes[:, : dt.n_splines] = coef.to(tdt)
+    ratios = torch.empty((P, S), dtype=torch.float64, device=device)
+    if P == 0:
+        return ratios
+    L = _abi.load()
+    ws_bytes = int(L.spo_eval_ratios_workspace_bytes(kind.code, dt.dtype_code, dt.nb, dt.n_tiles, P))
+    if ws_bytes < 0:
+        raise ConfigError("the ratio epilogue needs table rows of a multiple of 512 bytes "
+                          f"(tile of {512 // dt.dtype.itemsize} lanes); got nb={dt.nb}")
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
+    own_status = status is None and check
+    if own_status:
+        status = torch.zeros(1, dtype=torch.int32, device=device)
+    g = dt.grid
+    _abi.check(L.spo_eval_ratios(
+        kind.code, dt.dtype_code, dt.data.data_ptr(), _abi.i32x3(g.counts), dt.nb, dt.n_tiles,
+        _abi.f64x3(g.inverse_spacings), _abi.f64x3(g.spacings), pos.data_ptr(), P, lanes.data_ptr(),
+        lanes.stride(0), ratios.data_ptr(), status.data_ptr() if status is not None else None,
+        ws.data_ptr(), ws_bytes, _stream_ptr(device)))
+    if own_status and int(status.item()) != 0:
+        raise DomainError("positions contain non-finite components")
+    return ratios
 
 
 def streams(result, table, kind) -> dict:

@@ -34,7 +34,9 @@ def test_library_exports_every_header_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.spo_abi_version() == 2
+    assert lib.spo_abi_version() == 3
+    assert lib.spo_eval_ratios_workspace_bytes(2, 0, 128, 32, 1000) > 1000 * 160 + 32 * 1000 * 10 * 8 - 1
+    assert lib.spo_eval_ratios_workspace_bytes(2, 0, 96, 1, 1000) == -1  # 384-byte rows
     assert lib.spo_eval_workspace_bytes(2, 0, 0, 1000) >= 1000 * 160
     assert lib.spo_eval_workspace_bytes(2, 1, 0, 1000) >= 1000 * 304  # fp64 records
     assert lib.spo_eval_workspace_bytes(2, 0, 1, 1000) == 0  # strict: generic kernel only

@@ -1,0 +1,67 @@
+"""Fused consumer epilogue (evaluate_ratios): the per-position contraction of
+every output stream with a coefficient row equals the same contraction of
+evaluate()'s outputs, for fp32 and fp64 tables, tiled and not; deterministic."""
+import numpy as np
+import pytest
+
+from paper_1611_02665_b200 import ConfigError, DeviceTable, DomainError, evaluate, evaluate_ratios, streams
+from paper_1611_02665_b200.grid import GridSpec, unit_cell_grid
+from paper_1611_02665_b200.kernels import KernelKind
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+
+    assert t.cuda.is_available()
+    return t
+
+
+def reference_ratios(torch, dt, kind, pos, coef):
+    out = evaluate(dt, kind, pos, pipeline=True)
+    s = streams(out, dt, kind)
+    names = KernelKind(kind).stream_names
+    full = torch.stack([s[k].double() for k in names], dim=1)  # [P][S][N]
+    return torch.einsum("psn,pn->ps", full, coef.double())
+
+
+@pytest.mark.parametrize("kind", ["v", "vgl", "vgh"])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_ratios_match_contracted_outputs(torch, kind, dtype):
+    grid = unit_cell_grid(20)
+    rng = np.random.default_rng(5)
+    if dtype == "f32":
+        dt = DeviceTable.random(grid, 300, seed=2, tile_size=128)
+        tdt = torch.float32
+        rtol = 1e-6
+    else:
+        dt = DeviceTable.normal_f64(grid, 200, seed=2, tile_size=64)
+        tdt = torch.float64
+        rtol = 1e-12
+    pos = rng.random((5000, 3)) * 2.0 - 0.5
+    coef = torch.from_numpy(rng.standard_normal((5000, dt.n_splines))).to("cuda", tdt)
+    got = evaluate_ratios(dt, kind, pos, coef)
+    want = reference_ratios(torch, dt, kind, pos, coef)
+    scale = want.abs().max()
+    assert float((got - want).abs().max() / scale) < rtol
+    again = evaluate_ratios(dt, kind, pos, coef)
+    assert torch.equal(got, again)  # fixed-order reduction: bitwise reproducible
+
+
+def test_ratios_untiled_and_errors(torch):
+    grid = GridSpec(12, 13, 14, 0.1, 0.2, 0.3)
+    dt = DeviceTable.random(grid, 256, seed=1, tile_size=None)  # 1 KB rows: two 512-byte chunks
+    pos = np.random.default_rng(1).random((777, 3)) * 3.0
+    coef = torch.ones((777, 256), dtype=torch.float32, device="cuda")
+    got = evaluate_ratios(dt, "vgh", pos, coef)
+    want = reference_ratios(torch, dt, "vgh", pos, coef)
+    assert float((got - want).abs().max() / want.abs().max()) < 1e-6
+    odd = DeviceTable.random(grid, 96, seed=1, tile_size=None)  # 384-byte rows
+    with pytest.raises(ConfigError):
+        evaluate_ratios(odd, "v", pos, torch.ones((777, 96), device="cuda"))
+    bad = pos.copy()
+    bad[3, 0] = np.nan
+    with pytest.raises(DomainError):
+        evaluate_ratios(dt, "v", bad, coef)
