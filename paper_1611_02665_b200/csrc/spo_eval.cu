@@ -220,8 +220,8 @@ __device__ __forceinline__ void contract_strict(const float *__restrict__ rp, lo
 }
 
 // -------------------------------------------------------------- kernel ----
-template <int KIND, typename T, bool STRICT, int MINB>
-__global__ void __launch_bounds__(256, MINB) eval_kernel(const EvalArgs a) {
+template <int KIND, typename T, bool STRICT>
+__global__ void __launch_bounds__(256, 1) eval_kernel(const EvalArgs a) {
     constexpr int W = Vec<T>::W;
     constexpr int S = Streams<KIND>::S;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -279,11 +279,7 @@ __global__ void __launch_bounds__(256, MINB) eval_kernel(const EvalArgs a) {
 
 template <int KIND, typename T, bool STRICT>
 static int launch(const EvalArgs &a, dim3 grid, dim3 block, size_t smem, cudaStream_t st) {
-    static const int minb = getenv("SPO_MINB") ? atoi(getenv("SPO_MINB")) : 1;
-    if (minb >= 2)
-        eval_kernel<KIND, T, STRICT, 2><<<grid, block, smem, st>>>(a);
-    else
-        eval_kernel<KIND, T, STRICT, 1><<<grid, block, smem, st>>>(a);
+    eval_kernel<KIND, T, STRICT><<<grid, block, smem, st>>>(a);
     return check_launch("spo_eval launch");
 }
 
