@@ -64,7 +64,8 @@ struct Args {
     const unsigned char *recs;  // [n_pos][RECB] bucket-sorted
     unsigned *ticket;
     long long n_pos;
-    long long nbatch;           // ceil(n_pos / BP)
+    long long nbatch;           // ceil(n_pos / bp)
+    int bp;                     // positions per item (<= BP; small batches use fewer)
     long long n_items;          // units * nbatch
     int chunks;                 // chunks of CW lanes per tile row
     int nb;                     // table row length (lanes)
@@ -488,8 +489,8 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
                 const long long b = (long long)k - u * a.nbatch;
                 it.m = (int)(u / a.chunks);
                 it.c = (int)(u - (long long)it.m * a.chunks);
-                it.b0 = b * BP;
-                it.nb = (int)min((long long)BP, a.n_pos - it.b0);
+                it.b0 = b * a.bp;
+                it.nb = (int)min((long long)a.bp, a.n_pos - it.b0);
                 it.G = (it.nb + PW - 1) / PW;
                 if (a.proxy_fence) fence_proxy_async();  // WAR on the slot, see issue()
                 mbar_arrive_expect_tx(&rbar[slot], (unsigned)(it.nb * RECB));
@@ -673,8 +674,7 @@ template <int KIND, typename T, int CW, bool RATIO>
 static int launch_t(const CUtensorMap &map, const Args &a, int sms, cudaStream_t st) {
     using C = typename TT<T>::Cfg;
     constexpr size_t sm = smem_bytes<T>();
-    const long long warps_needed = (a.n_items + 1) / 2;
-    int grid = (int)min((long long)sms, (warps_needed + C::WARPS - 1) / C::WARPS);
+    int grid = (int)min((long long)sms, (a.n_items + C::WARPS - 1) / C::WARPS);
     if (grid < 1) grid = 1;
     cudaFuncSetAttribute(eval_tma_kernel<KIND, T, CW, C, RATIO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
@@ -713,6 +713,8 @@ __global__ void ratio_reduce_kernel(const double *__restrict__ partials, long lo
         ratios[e] = s;
     }
 }
+
+constexpr long long ITEMS_PER_WARP_SMALL = 16, ITEMS_PER_WARP_FULL = 96;
 
 static int rec_bytes(int dtype) { return dtype == SPO_F64 ? TT<double>::RECB : TT<float>::RECB; }
 static int item_positions(int dtype) { return dtype == SPO_F64 ? TT<double>::Cfg::BP : TT<float>::Cfg::BP; }
@@ -782,10 +784,23 @@ int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const
                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    {
-        const long long nbatch = (n_pos + item_positions(dtype) - 1) / item_positions(dtype);
-        if (nbatch * (long long)geo.n_tiles * (geo.nb / cw) >= (1LL << 32)) return -1;  // 32-bit tickets
-    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long units = (long long)geo.n_tiles * (geo.nb / cw);
+    const int BP = item_positions(dtype);
+    const int pw = 32 * (16 / E) / cw;  // positions per warp step
+    const long long warps = (long long)sms * (dtype == SPO_F64 ? TT<double>::Cfg::WARPS : TT<float>::Cfg::WARPS);
+    // Item size: BP positions when every warp gets many items, fewer when it
+    // gets few.  Measured (scripts/micro/item_size.py, interleaved medians):
+    // smaller items cut the dynamic-scheduling tail and keep the in-flight
+    // window inside fewer units (smaller L2 working set); at full size the
+    // ticket and record traffic of small items costs more than that.
+    const long long per_warp = units * ((n_pos + BP - 1) / BP) / warps;
+    int bp = per_warp < ITEMS_PER_WARP_SMALL ? 2 : (per_warp < ITEMS_PER_WARP_FULL ? 4 : BP);
+    bp = max(bp, pw);
+    if (getenv("SPO_BP")) bp = max(1, min(BP, atoi(getenv("SPO_BP"))));
+    if (((n_pos + bp - 1) / bp) * units >= (1LL << 32)) return -1;  // 32-bit tickets
 
     unsigned char *ws = static_cast<unsigned char *>(workspace);
     unsigned *counts = reinterpret_cast<unsigned *>(ws + 256);
@@ -807,12 +822,12 @@ int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const
         if (rc) return rc;
     }
 
-    const int BP = item_positions(dtype);
     Args a;
     a.recs = recs;
     a.ticket = reinterpret_cast<unsigned *>(ws);
     a.n_pos = n_pos;
-    a.nbatch = (n_pos + BP - 1) / BP;
+    a.bp = bp;
+    a.nbatch = (n_pos + bp - 1) / bp;
     a.chunks = geo.nb / cw;
     a.n_items = a.nbatch * (long long)geo.n_tiles * a.chunks;
     a.nb = geo.nb;
@@ -828,9 +843,6 @@ int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const
     a.coef_stride = coef_stride;
     a.partials = ratio ? reinterpret_cast<double *>(ws + eval_tma_workspace_bytes(dtype, n_pos)) : nullptr;
 
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int rc = dtype == SPO_F64 ? launch_kind<double>(kind, cwb, ratio, map, a, sms, st)
                                     : launch_kind<float>(kind, cwb, ratio, map, a, sms, st);
     if (rc || !ratio) return rc;

@@ -195,8 +195,8 @@ def _positions_tensor(positions, device):
 
 
 # positions x lanes from which the TMA-pipelined kernel beats the generic one
-# (scripts/micro/small_batch.py: crossover ~2^20 for N = 64 ... 4096)
-PIPELINE_MIN_WORK = 1 << 20
+# (scripts/micro/small_batch.py: crossover ~2^19 for N = 64 ... 4096)
+PIPELINE_MIN_WORK = 1 << 19
 
 
 def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=None,

@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Per-call latency of evaluate() vs batch size, TMA-pipelined vs generic
-kernel (decides the small-batch cutover in kernels.evaluate)."""
+kernel, eager and CUDA-graph replayed (decides the small-batch cutover in
+kernels.evaluate)."""
 import json
 import os
 import sys
@@ -14,6 +15,7 @@ def main():
     import torch
 
     from paper_1611_02665_b200 import DeviceTable, evaluate
+    from paper_1611_02665_b200.graphs import GraphedEvaluator
     from paper_1611_02665_b200.grid import unit_cell_grid
 
     for n_grid, n in ((16, 64), (48, 512), (64, 4096)):
@@ -34,6 +36,16 @@ def main():
                 e1.record()
                 e1.synchronize()
                 res["tma" if pipe else "generic"] = e0.elapsed_time(e1) / reps * 1e3
+                g = GraphedEvaluator(dt, "vgh", P, pipeline=pipe)
+                for _ in range(3):
+                    g.run(pos)
+                torch.cuda.synchronize()
+                e0.record()
+                for _ in range(reps):
+                    g.run(pos)
+                e1.record()
+                e1.synchronize()
+                res[("tma" if pipe else "generic") + "_graph"] = e0.elapsed_time(e1) / reps * 1e3
             print(json.dumps({"grid": n_grid, "N": n, "P": P, "us_per_call": res}), flush=True)
 
 
