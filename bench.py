@@ -154,7 +154,7 @@ def workload(args, rank):
     return cfg, kind, pos, bytes_per_position(kind, cfg.n_splines)
 
 
-def cpu_baseline(table_soa, grid, kind, pos, n_splines, budget_s, threads=0):
+def cpu_baseline(table_soa, grid, kind, pos, n_splines, budget_s, threads=0, one_thread_s=0.0):
     """Reference fp32 kernels restated in C (oracle/), all host threads, with
     the reference's batch semantics (each thread overwrites its own output
     buffer, kernels.py:353-354).  Calibrated to ~budget_s of CPU work."""
@@ -175,10 +175,16 @@ def cpu_baseline(table_soa, grid, kind, pos, n_splines, budget_s, threads=0):
     t0 = time.perf_counter()
     oracle.eval_f32(kind, table_soa, spac, pos[:n_final], overwrite=True, nthreads=threads)
     dt = time.perf_counter() - t0
-    return {"value": n_final * n_splines / dt, "unit": UNIT, "cores": threads, "kind": "port",
+    res = {"value": n_final * n_splines / dt, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{n_final} of the workload's positions x N={n_splines} {kind.upper()}, "
                       f"{dt:.1f} s, C restatement of kernels.py fp32 kernels (oracle/spline_oracle.c, "
                       f"-O3 AVX2/AVX-512 clones, OpenMP)"}
+    if threads > 1 and one_thread_s > 0:  # report 1-thread and all-core figures
+        n1 = max(1, int(n_final / threads * one_thread_s / max(dt, 1e-6)))
+        t0 = time.perf_counter()
+        oracle.eval_f32(kind, table_soa, spac, pos[:n1], overwrite=True, nthreads=1)
+        res["value_1thread"] = n1 * n_splines / (time.perf_counter() - t0)
+    return res
 
 
 def host_reference_table(cfg, seed=0):
@@ -359,7 +365,7 @@ def run_b200(args):
         dist.barrier()
     if rank == 0 and world == 1 and not args.no_cpu:
         soa = table.reference_soa()
-        result["cpu_baseline"] = cpu_baseline(soa, cfg.grid, kind, pos_np, N, args.cpu_seconds)
+        result["cpu_baseline"] = cpu_baseline(soa, cfg.grid, kind, pos_np, N, args.cpu_seconds, one_thread_s=3.0)
         del soa
     if rank == 0:
         print(json.dumps(result), flush=True)
