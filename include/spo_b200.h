@@ -60,7 +60,7 @@
 extern "C" {
 #endif
 
-#define SPO_ABI_VERSION 3
+#define SPO_ABI_VERSION 4
 
 /* kernel kinds: KernelKind (kernels.py:26-51) */
 #define SPO_KIND_V 0
@@ -106,6 +106,24 @@ int spo_eval(int kind, int dtype, int mode, const void *table, const int32_t *n3
              int64_t n_pos, void *out, int64_t out_pos_stride, int64_t out_stream_stride,
              const int64_t *out_index, int32_t *status, void *workspace, int64_t workspace_bytes,
              void *stream);
+
+/*
+ * spo_eval writing only output lanes [0, lane_limit) (1 <= lane_limit <= the
+ * table's lanes) into `out`, which may live on ANOTHER GPU: the launch device
+ * is the table's, and `out` may be peer memory it can reach (same process:
+ * peer access is enabled here; another process: an IPC mapping).  This is
+ * the fused evaluate + gather of the orbital-sharded mode:
+ * rank r passes root_out + lo_r with lane_limit = its n_r splines and the
+ * root's strides, so its kernel's output stores travel over NVLink straight
+ * into the root's [P][S][N] buffer -- no gather buffer, no collective, no
+ * permute.  Lanes must equal spline indices (untiled table, or tiles with no
+ * padding lanes); out + lane stores need the usual 16-byte alignment.
+ */
+int spo_eval_lanes(int kind, int dtype, int mode, const void *table, const int32_t *n3, int32_t nb,
+                   int32_t n_tiles, const double *dinv3, const double *delta3, const double *pos,
+                   int64_t n_pos, void *out, int64_t out_pos_stride, int64_t out_stream_stride,
+                   int64_t lane_limit, const int64_t *out_index, int32_t *status, void *workspace,
+                   int64_t workspace_bytes, void *stream);
 
 /* Workspace spo_eval wants for this request (0 = none used, -1 = bad args). */
 int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64_t n_pos);

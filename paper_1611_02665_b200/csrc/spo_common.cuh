@@ -70,6 +70,35 @@ inline int check_on_device(const void *ptr, const char *what) {
     return SPO_OK;
 }
 
+// `out` of spo_eval_lanes: memory of the current device, or of a peer the
+// current device can reach over NVLink/PCIe (peer access is enabled here; an
+// IPC mapping opened with lazy peer access is already reachable).
+inline int check_reachable(const void *ptr, const char *what) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SPO_ERR_CONTRACT, "%s (%p) is not a CUDA allocation", what, ptr);
+    }
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+        return fail(SPO_ERR_CONTRACT, "%s (%p) is not device memory", what, ptr);
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (at.device == cur || at.type == cudaMemoryTypeManaged) return SPO_OK;
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, cur, at.device) != cudaSuccess || !can) {
+        cudaGetLastError();
+        return fail(SPO_ERR_CONTRACT, "%s (%p) lives on device %d, which device %d cannot reach", what, ptr,
+                    at.device, cur);
+    }
+    const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return fail(SPO_ERR_CUDA, "cudaDeviceEnablePeerAccess(%d) from %d failed", at.device, cur);
+    }
+    cudaGetLastError();
+    return SPO_OK;
+}
+
 inline int check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SPO_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));

@@ -83,6 +83,7 @@ struct EvalArgs {
     void *out;
     long long out_pos_stride, out_stream_stride;
     const long long *out_index;
+    long long lane_limit;  // output lanes >= lane_limit are not stored
     int *status;
 };
 
@@ -272,8 +273,17 @@ __global__ void __launch_bounds__(256, 1) eval_kernel(const EvalArgs a) {
         }
         const long long op = a.out_index ? a.out_index[p0 + q] : p0 + q;
         T *o = reinterpret_cast<T *>(a.out) + op * a.out_pos_stride + lane0;
+        if (lane0 + W <= a.lane_limit) {
 #pragma unroll
-        for (int s = 0; s < S; ++s) st16(o + s * a.out_stream_stride, acc[s]);
+            for (int s = 0; s < S; ++s) st16(o + s * a.out_stream_stride, acc[s]);
+        } else if (lane0 < a.lane_limit) {  // the vector straddles lane_limit
+            const int nv = (int)(a.lane_limit - lane0);
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int e = 0; e < W - 1; ++e)
+                    if (e < nv) o[s * a.out_stream_stride + e] = acc[s][e];
+        }
     }
 }
 
@@ -288,8 +298,8 @@ static int launch(const EvalArgs &a, dim3 grid, dim3 block, size_t smem, cudaStr
 namespace spo {
 int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const GridArgs &g, const double *pos,
              long long n_pos, void *out, long long ops, long long oss, const long long *out_index, int *status,
-             void *workspace, long long ws_bytes, cudaStream_t st, int cw_request, const void *coef = nullptr,
-             long long coef_stride = 0, double *ratios = nullptr);
+             void *workspace, long long ws_bytes, cudaStream_t st, int cw_request, long long lane_limit,
+             const void *coef = nullptr, long long coef_stride = 0, double *ratios = nullptr);
 long long eval_tma_workspace_bytes(int dtype, long long n_pos);
 long long eval_tma_ratio_bytes(int kind, int dtype, long long nb, long long n_tiles, long long n_pos);
 }
@@ -306,11 +316,15 @@ extern "C" int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64
     return eval_tma_workspace_bytes(dtype, n_pos);
 }
 
-extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const int32_t *n3,
-                        int32_t nb, int32_t n_tiles, const double *dinv3, const double *delta3,
-                        const double *pos, int64_t n_pos, void *out, int64_t out_pos_stride,
-                        int64_t out_stream_stride, const int64_t *out_index, int32_t *status,
-                        void *workspace, int64_t workspace_bytes, void *stream) {
+// lane_limit < 0: every table lane is stored and `out` must be memory of the
+// launch device (bound from `out`).  lane_limit >= 0 (spo_eval_lanes): lanes
+// [0, lane_limit) are stored, the launch device is the table's and `out` may
+// be peer memory reachable from it.
+static int eval_impl(int kind, int dtype, int mode, const void *table, const int32_t *n3, int32_t nb,
+                     int32_t n_tiles, const double *dinv3, const double *delta3, const double *pos, int64_t n_pos,
+                     void *out, int64_t out_pos_stride, int64_t out_stream_stride, int64_t lane_limit,
+                     const int64_t *out_index, int32_t *status, void *workspace, int64_t workspace_bytes,
+                     void *stream) {
     if (kind < SPO_KIND_V || kind > SPO_KIND_VGH) return fail(SPO_ERR_CONTRACT, "unknown kind %d", kind);
     if (dtype != SPO_F32 && dtype != SPO_F64) return fail(SPO_ERR_CONTRACT, "unknown dtype %d", dtype);
     if (mode != SPO_MODE_FAST && mode != SPO_MODE_STRICT) return fail(SPO_ERR_CONTRACT, "unknown mode %d", mode);
@@ -328,7 +342,11 @@ extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const 
         return fail(SPO_ERR_CONTRACT, "table and out must be 16-byte aligned");
     if (out_pos_stride % W || out_stream_stride % W)
         return fail(SPO_ERR_CONTRACT, "output strides must be multiples of %d elements", W);
-    const long long lanes = (long long)nb * n_tiles;
+    const bool peer = lane_limit >= 0;
+    const long long table_lanes = (long long)nb * n_tiles;
+    if (peer && (lane_limit == 0 || lane_limit > table_lanes))
+        return fail(SPO_ERR_CONTRACT, "lane_limit %lld outside [1, %lld]", (long long)lane_limit, table_lanes);
+    const long long lanes = peer ? (long long)lane_limit : table_lanes;
     if (S > 1 && out_stream_stride < lanes)
         return fail(SPO_ERR_CONTRACT, "out_stream_stride %lld shorter than the %lld table lanes",
                     (long long)out_stream_stride, lanes);
@@ -339,11 +357,12 @@ extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const 
         if (!(dinv3[ax] > 0.0) || !(delta3[ax] > 0.0))
             return fail(SPO_ERR_CONFIG, "grid spacing on axis %d must be positive", ax);
 
-    rc = bind_device(out);
+    rc = peer ? bind_device(table) : bind_device(out);
     if (rc) return rc;
     if ((rc = check_on_device(table, "table")) || (rc = check_on_device(pos, "positions")) ||
         (rc = check_on_device(out_index, "out_index")) || (rc = check_on_device(status, "status")) ||
-        (rc = check_on_device(workspace, "workspace")))
+        (rc = check_on_device(workspace, "workspace")) ||
+        (rc = peer ? check_reachable(out, "out") : SPO_OK))
         return rc;
     if (mode == SPO_MODE_FAST) {
         static const char *env_tma = getenv("SPO_TMA");
@@ -359,7 +378,7 @@ extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const 
             const int r = eval_tma(kind, dtype, table, geo, g, pos, n_pos, out, out_pos_stride, out_stream_stride,
                                    reinterpret_cast<const long long *>(out_index), status, workspace,
                                    workspace_bytes, reinterpret_cast<cudaStream_t>(stream),
-                                   env_cw ? atoi(env_cw) : 0);
+                                   env_cw ? atoi(env_cw) : 0, lanes);
             if (r >= 0) return r;
         }
     }
@@ -391,6 +410,7 @@ extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const 
     a.out_pos_stride = out_pos_stride;
     a.out_stream_stride = out_stream_stride;
     a.out_index = reinterpret_cast<const long long *>(out_index);
+    a.lane_limit = lanes;
     a.status = status;
 
     const int groups = 256 / chv;
@@ -427,6 +447,25 @@ extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const 
         case SPO_KIND_VGL: return launch<SPO_KIND_VGL, float, false>(a, grid, block, smem, st);
         default: return launch<SPO_KIND_VGH, float, false>(a, grid, block, smem, st);
     }
+}
+
+extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const int32_t *n3,
+                        int32_t nb, int32_t n_tiles, const double *dinv3, const double *delta3,
+                        const double *pos, int64_t n_pos, void *out, int64_t out_pos_stride,
+                        int64_t out_stream_stride, const int64_t *out_index, int32_t *status,
+                        void *workspace, int64_t workspace_bytes, void *stream) {
+    return eval_impl(kind, dtype, mode, table, n3, nb, n_tiles, dinv3, delta3, pos, n_pos, out, out_pos_stride,
+                     out_stream_stride, -1, out_index, status, workspace, workspace_bytes, stream);
+}
+
+extern "C" int spo_eval_lanes(int kind, int dtype, int mode, const void *table, const int32_t *n3,
+                              int32_t nb, int32_t n_tiles, const double *dinv3, const double *delta3,
+                              const double *pos, int64_t n_pos, void *out, int64_t out_pos_stride,
+                              int64_t out_stream_stride, int64_t lane_limit, const int64_t *out_index,
+                              int32_t *status, void *workspace, int64_t workspace_bytes, void *stream) {
+    if (lane_limit < 0) return fail(SPO_ERR_CONTRACT, "lane_limit %lld < 0", (long long)lane_limit);
+    return eval_impl(kind, dtype, mode, table, n3, nb, n_tiles, dinv3, delta3, pos, n_pos, out, out_pos_stride,
+                     out_stream_stride, lane_limit, out_index, status, workspace, workspace_bytes, stream);
 }
 
 // ------------------------------------------------------------ ratios ----
@@ -475,7 +514,7 @@ extern "C" int spo_eval_ratios(int kind, int dtype, const void *table, const int
         g.n[ax] = n3[ax];
     }
     rc = eval_tma(kind, dtype, table, geo, g, pos, n_pos, nullptr, 0, 0, nullptr, status, workspace,
-                  workspace_bytes, reinterpret_cast<cudaStream_t>(stream), 0, coef, coef_stride, ratios);
+                  workspace_bytes, reinterpret_cast<cudaStream_t>(stream), 0, 0, coef, coef_stride, ratios);
     if (rc < 0) return fail(SPO_ERR_CONFIG, "the fused ratio epilogue is unavailable for this request");
     return rc;
 }

@@ -72,6 +72,7 @@ struct Args {
     void *out;
     long long out_pos_stride, out_stream_stride;
     const long long *out_index;
+    long long lane_limit;       // output lanes >= lane_limit are not stored
     int evict_last;             // L2 evict_last hint on table slabs
     int proxy_fence;            // fence.proxy.async before reusing a stage (diagnostic)
     // fused ratio epilogue (RATIO kernels): per (unit, position) partial dot
@@ -297,6 +298,25 @@ __device__ __forceinline__ void store_lane(double *o, long long sstride, const d
 #pragma unroll
     for (int s = 0; s < S; ++s)
         __stcs(reinterpret_cast<double2 *>(o + s * sstride), finite ? acc[s][0] : make_double2(NAN, NAN));
+}
+// the lane vector straddles lane_limit: store its first `nv` lanes only
+// (unrolled + predicated: no dynamic indexing of the accumulators)
+template <int S>
+__device__ __forceinline__ void store_lane_partial(float *o, long long sstride, const float2 (&acc)[S][2],
+                                                   bool finite, int nv) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        if (nv > 0) o[s * sstride + 0] = finite ? acc[s][0].x : NAN;
+        if (nv > 1) o[s * sstride + 1] = finite ? acc[s][0].y : NAN;
+        if (nv > 2) o[s * sstride + 2] = finite ? acc[s][1].x : NAN;
+    }
+}
+template <int S>
+__device__ __forceinline__ void store_lane_partial(double *o, long long sstride, const double2 (&acc)[S][1],
+                                                   bool finite, int nv) {
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+        if (nv > 0) o[s * sstride] = finite ? acc[s][0].x : NAN;
 }
 
 // ------------------------------------------------------------ prologue --
@@ -629,9 +649,12 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
             } else if (p < it.nb) {
                 const long long gp = cell.w;  // original index
                 const long long op = a.out_index ? a.out_index[gp] : gp;
-                T *o = reinterpret_cast<T *>(a.out) + op * a.out_pos_stride + (long long)it.m * a.nb + it.c * CW +
-                       vl * W;
-                store_lane<S>(o, a.out_stream_stride, acc, cell.x >= 0);
+                const long long lane = (long long)it.m * a.nb + it.c * CW + vl * W;
+                T *o = reinterpret_cast<T *>(a.out) + op * a.out_pos_stride + lane;
+                if (lane + W <= a.lane_limit)
+                    store_lane<S>(o, a.out_stream_stride, acc, cell.x >= 0);
+                else if (lane < a.lane_limit)
+                    store_lane_partial<S>(o, a.out_stream_stride, acc, cell.x >= 0, (int)(a.lane_limit - lane));
             }
         }
         __syncwarp();
@@ -744,8 +767,8 @@ long long eval_tma_ratio_bytes(int kind, int dtype, long long nb, long long n_ti
 // stream_s(p, n) * coef[p][lane(n)] in fp64 (coef in output-lane layout).
 int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const GridArgs &g, const double *pos,
              long long n_pos, void *out, long long ops, long long oss, const long long *out_index, int *status,
-             void *workspace, long long ws_bytes, cudaStream_t st, int cw_request, const void *coef = nullptr,
-             long long coef_stride = 0, double *ratios = nullptr) {
+             void *workspace, long long ws_bytes, cudaStream_t st, int cw_request, long long lane_limit,
+             const void *coef = nullptr, long long coef_stride = 0, double *ratios = nullptr) {
     using namespace tma;
     const bool ratio = ratios != nullptr;
     const long long partial_bytes = ratio ? eval_tma_ratio_bytes(kind, dtype, geo.nb, geo.n_tiles, n_pos) : 0;
@@ -835,6 +858,7 @@ int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const
     a.out_pos_stride = ops;
     a.out_stream_stride = oss;
     a.out_index = out_index;
+    a.lane_limit = lane_limit;
     static const char *env_hint = getenv("SPO_L2HINT");
     a.evict_last = !(env_hint && env_hint[0] == '0');
     static const char *env_fence = getenv("SPO_PROXY_FENCE");

@@ -127,6 +127,12 @@ class DeviceTable:
         n = np.asarray(n)
         return (n // self.tile_size) * self.nb + n % self.tile_size
 
+    @property
+    def lanes_are_splines(self) -> bool:
+        """Output lane n holds spline n for every n < N (untiled, or tiles
+        without padding lanes): the layout spo_eval_lanes needs."""
+        return self.n_tiles == 1 or self.tile_size == self.nb
+
     def lane_index(self):
         """int64 tensor of the lanes of splines 0..N-1 (for compaction)."""
         torch = _torch()

@@ -200,7 +200,7 @@ PIPELINE_MIN_WORK = 1 << 19
 
 
 def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=None,
-             status=None, check: bool = True, pipeline="auto"):
+             status=None, check: bool = True, pipeline="auto", lane_limit=None):
     """Evaluate `kind` at every position; returns out[P][S][lanes] (CUDA).
 
     table      DeviceTable (or any host table -> uploaded once and cached)
@@ -213,6 +213,10 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
     pipeline   fp32 fast mode: True = TMA-pipelined kernel (needs a workspace,
                allocated here), False = the generic kernel (same bits),
                "auto" = pipelined when P * lanes >= PIPELINE_MIN_WORK
+    lane_limit store only output lanes [0, lane_limit) (spo_eval_lanes); `out`
+               is then required and may live on another GPU (a peer
+               device's memory or an IPC mapping of it): the fused
+               evaluate + gather of multi.PeerGather
     """
     torch = _torch()
     kind = as_kind(kind)
@@ -222,7 +226,19 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
     P = pos.shape[0]
     S = kind.output_streams_soa
     tdt = torch.float64 if dt.dtype == np.float64 else torch.float32
-    if out is None:
+    if lane_limit is not None:
+        lane_limit = int(lane_limit)
+        if out is None:
+            raise ContractError("lane_limit needs a preallocated out tensor")
+        if not 1 <= lane_limit <= dt.lanes:
+            raise ContractError(f"lane_limit {lane_limit} outside [1, {dt.lanes}]")
+        if out.dtype != tdt or not out.is_cuda:
+            raise ContractError("out must be a CUDA tensor of the table dtype")
+        if out.dim() != 3 or out.shape[1] != S or out.shape[2] < lane_limit or out.stride(2) != 1:
+            raise ContractError(f"out must be [P][{S}][>={lane_limit}] with unit lane stride")
+        if out_index is None and out.shape[0] < P:
+            raise ContractError(f"out holds {out.shape[0]} positions, need {P}")
+    elif out is None:
         out = torch.empty((P, S, dt.lanes), dtype=tdt, device=device)
     else:
         if out.dtype != tdt or out.device != device:
@@ -251,12 +267,15 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
         pipeline = P * dt.lanes >= PIPELINE_MIN_WORK
     ws_bytes = int(L.spo_eval_workspace_bytes(kind.code, dt.dtype_code, _MODES[mode], P)) if pipeline else 0
     ws = torch.empty(max(ws_bytes, 0), dtype=torch.uint8, device=device) if ws_bytes > 0 else None
-    _abi.check(L.spo_eval(
-        kind.code, dt.dtype_code, _MODES[mode], dt.data.data_ptr(), _abi.i32x3(g.counts), dt.nb,
-        dt.n_tiles, _abi.f64x3(g.inverse_spacings), _abi.f64x3(g.spacings), pos.data_ptr(), P,
-        out.data_ptr(), out.stride(0), out.stride(1), idx_ptr,
-        status.data_ptr() if status is not None else None,
-        ws.data_ptr() if ws is not None else None, max(ws_bytes, 0), _stream_ptr(device)))
+    head = (kind.code, dt.dtype_code, _MODES[mode], dt.data.data_ptr(), _abi.i32x3(g.counts), dt.nb,
+            dt.n_tiles, _abi.f64x3(g.inverse_spacings), _abi.f64x3(g.spacings), pos.data_ptr(), P,
+            out.data_ptr(), out.stride(0), out.stride(1))
+    tail = (idx_ptr, status.data_ptr() if status is not None else None,
+            ws.data_ptr() if ws is not None else None, max(ws_bytes, 0), _stream_ptr(device))
+    if lane_limit is None:
+        _abi.check(L.spo_eval(*head, *tail))
+    else:
+        _abi.check(L.spo_eval_lanes(*head, lane_limit, *tail))
     if own_status and int(status.item()) != 0:
         raise DomainError("positions contain non-finite components")
     return out

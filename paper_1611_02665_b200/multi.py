@@ -8,9 +8,11 @@ Two modes, both without a collective on the evaluation path:
 * orbital-sharded -- the reference's nested tile parallelism (driver.py:349-434,
   tile_table coeffs.py:197-210) across GPUs: rank r holds splines
   [lo_r, hi_r) and evaluates every position for that slice.  Only when the
-  caller needs full-N outputs on one device are the slices gathered along N
-  with NCCL (all-gather into [world][P][S][n_max] + a local permute), which is
-  the one exchange step of the path.
+  caller needs full-N outputs on one device are the slices gathered along N,
+  the one exchange step of the path: fused into the kernel's own output
+  stores over peer memory (PeerGather, spo_eval_lanes), or with NCCL
+  (gather_orbital_blocks: all-gather into [world][P][S][n_max] + a local
+  permute) as the baseline.
 
 The partition/gather helpers take plain tensors so they also run on CPU with
 the gloo backend (tests/test_multi_gloo.py); the evaluation itself is the
@@ -137,6 +139,103 @@ def evaluate_orbital_sharded(local_table, kind, positions, part: OrbitalPartitio
         block = local[:, :, : local_table.n_splines]
     full = gather_orbital_blocks(block, part, group=group, root=root)
     return full, local
+
+
+def _lane_quantum(dtype) -> int:
+    """Output lanes per 16-byte store (fp32: 4, fp64: 2)."""
+    return 16 // np.dtype(dtype).itemsize
+
+
+def check_peer_partition(part: OrbitalPartition, dtype) -> None:
+    """Every rank's first spline must start a 16-byte lane vector of the
+    root's rows, so its stores stay aligned and never touch a neighbour's
+    lanes (the last lane vector of a slice is stored lane by lane)."""
+    q = _lane_quantum(dtype)
+    for r, (lo, _hi) in enumerate(part.bounds):
+        if lo % q:
+            raise ValueError(f"rank {r} starts at spline {lo}, not a multiple of {q}: "
+                             f"use OrbitalPartition.make(..., quantum={q}) or a multiple")
+
+
+class PeerGather:
+    """Fused evaluate + gather along N over peer memory (orbital-sharded mode,
+    SURVEY.md 8(e)).
+
+    The root allocates the full [capacity][S][Npad] output once and shares it
+    with every rank of `group` as a CUDA IPC handle (torch's CUDA tensor
+    reduction, sent with broadcast_object_list).  evaluate() then runs each
+    rank's kernel on its own GPU with spo_eval_lanes: the rank's spline slice
+    [lo, hi) is stored straight into the root's buffer at lane offset lo, so
+    the transfer rides on the kernel's own output stores over NVLink, overlapped
+    with the math tile by tile -- no gather buffer, no all-gather of padded
+    blocks, no permute (compare gather_orbital_blocks, the NCCL baseline).
+    Completion: every rank synchronises its stream, then a group barrier;
+    after it the root's view holds all N splines.  Kernels never wait on each
+    other.
+    """
+
+    def __init__(self, part: OrbitalPartition, kind, capacity: int, dtype, group=None, root: int = 0,
+                 device=None):
+        import torch
+        import torch.distributed as dist
+
+        from .kernels import as_kind
+
+        self.part, self.kind, self.group, self.root = part, as_kind(kind), group, root
+        self.dtype = np.dtype(dtype)
+        self.capacity = int(capacity)
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if world != part.world:
+            raise ValueError(f"partition has {part.world} ranks, group has {world}")
+        check_peer_partition(part, self.dtype)
+        q = _lane_quantum(self.dtype)
+        self.npad = -(-part.n_splines // q) * q
+        S = self.kind.output_streams_soa
+        tdt = torch.float64 if self.dtype == np.float64 else torch.float32
+        device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        handle = [None]
+        if self.rank == root:
+            self.buf = torch.empty((self.capacity, S, self.npad), dtype=tdt, device=device)
+            if world > 1:
+                from torch.multiprocessing.reductions import reduce_tensor
+
+                handle = [reduce_tensor(self.buf)]
+        if world > 1:
+            dist.broadcast_object_list(handle, src=root, group=group)
+            if self.rank != root:
+                fn, args = handle[0]
+                self.buf = fn(*args)  # IPC mapping of the root's buffer in this process
+
+    def evaluate(self, local_table, positions, **kw):
+        """Evaluate this rank's spline slice at every position into the root's
+        buffer.  Returns the root's [P][S][N] view on the root, None elsewhere."""
+        import torch
+        import torch.distributed as dist
+
+        from .device import as_device_table
+        from .errors import ContractError
+        from .kernels import _positions_tensor, evaluate
+
+        dt = as_device_table(local_table)
+        lo, hi = self.part.local(self.rank)
+        if dt.n_splines != hi - lo:
+            raise ContractError(f"rank {self.rank} table has {dt.n_splines} splines, partition says {hi - lo}")
+        if np.dtype(dt.dtype) != self.dtype:
+            raise ContractError("table dtype differs from the gather buffer's")
+        if not dt.lanes_are_splines:
+            raise ContractError("spo_eval_lanes needs lanes == spline indices (untiled, or tiles "
+                                "without padding lanes)")
+        pos = _positions_tensor(positions, dt.device)
+        P = pos.shape[0]
+        if P > self.capacity:
+            raise ContractError(f"{P} positions exceed the gather buffer's capacity {self.capacity}")
+        if hi > lo:
+            evaluate(dt, self.kind, pos, self.buf[:P, :, lo:], lane_limit=hi - lo, **kw)
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            torch.cuda.current_stream(dt.device).synchronize()
+            dist.barrier(group=self.group)
+        return self.buf[:P, :, : self.part.n_splines] if self.rank == self.root else None
 
 
 def shard_table_for_rank(full_table, part: OrbitalPartition, rank: int, tile_size=None):

@@ -34,7 +34,7 @@ def test_library_exports_every_header_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.spo_abi_version() == 3
+    assert lib.spo_abi_version() == 4
     assert lib.spo_eval_ratios_workspace_bytes(2, 0, 128, 32, 1000) > 1000 * 160 + 32 * 1000 * 10 * 8 - 1
     assert lib.spo_eval_ratios_workspace_bytes(2, 0, 96, 1, 1000) == -1  # 384-byte rows
     assert lib.spo_eval_workspace_bytes(2, 0, 0, 1000) >= 1000 * 160
@@ -65,6 +65,25 @@ def test_eval_argument_validation(lib):
     assert _eval(lib, n=0) == 0                                # empty batch: no-op
     assert _eval(lib, dinv=(0.0, 1.0, 1.0)) == 3
     assert b"positive" in lib.spo_last_error()
+
+
+def _eval_lanes(lib, limit, **kw):
+    a = dict(kind=2, dtype=0, mode=0, table=16, n3=(16, 16, 16), nb=64, n_tiles=1,
+             dinv=(16.0,) * 3, delta=(1 / 16,) * 3, pos=16, n=10, out=16, ps=640, ss=64)
+    a.update(kw)
+    return lib.spo_eval_lanes(a["kind"], a["dtype"], a["mode"], a["table"], _abi.i32x3(a["n3"]), a["nb"],
+                              a["n_tiles"], _abi.f64x3(a["dinv"]), _abi.f64x3(a["delta"]), a["pos"], a["n"],
+                              a["out"], a["ps"], a["ss"], limit, None, None, None, 0, None)
+
+
+def test_eval_lanes_argument_validation(lib):
+    assert _eval_lanes(lib, -1) == 1
+    assert _eval_lanes(lib, 0) == 1                 # at least one lane
+    assert _eval_lanes(lib, 65) == 1                # beyond the table's lanes
+    assert _eval_lanes(lib, 40, ss=32) == 1         # streams overlap the stored lanes
+    assert _eval_lanes(lib, 20, ss=20, ps=200, n=0) == 0  # empty batch: no-op
+    assert _eval_lanes(lib, 20, ss=22) == 1         # strides must be multiples of 4 lanes
+    assert b"multiples" in lib.spo_last_error()
 
 
 def test_error_codes_map_to_reference_exceptions(lib):
