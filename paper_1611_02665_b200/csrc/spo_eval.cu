@@ -301,6 +301,10 @@ int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const
              void *workspace, long long ws_bytes, cudaStream_t st, int cw_request, long long lane_limit,
              const void *coef = nullptr, long long coef_stride = 0, double *ratios = nullptr);
 long long eval_tma_workspace_bytes(int dtype, long long n_pos);
+long long eval_line_workspace_bytes(int dtype, long long n_pos);
+int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, const GridArgs &g, const double *pos,
+              long long n_pos, void *out, long long ops, long long oss, const long long *out_index, int *status,
+              void *workspace, long long ws_bytes, cudaStream_t st, long long lane_limit);
 long long eval_tma_ratio_bytes(int kind, int dtype, long long nb, long long n_tiles, long long n_pos);
 }
 
@@ -313,8 +317,13 @@ extern "C" const char *spo_last_error(void) { return last_error_slot().c_str(); 
 extern "C" int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64_t n_pos) {
     if (kind < SPO_KIND_V || kind > SPO_KIND_VGH || n_pos < 0) return -1;
     if ((dtype != SPO_F32 && dtype != SPO_F64) || mode != SPO_MODE_FAST) return 0;
-    return eval_tma_workspace_bytes(dtype, n_pos);
+    const long long a = eval_tma_workspace_bytes(dtype, n_pos), b = eval_line_workspace_bytes(dtype, n_pos);
+    return a > b ? a : b;
 }
+
+// positions per grid cell from which the line-window kernel is used (NUM/DEN):
+// sustained-rate crossover measured by scripts/micro/line_sustained.py
+constexpr long long LINE_DENSITY_NUM = 1, LINE_DENSITY_DEN = 2;
 
 // lane_limit < 0: every table lane is stored and `out` must be memory of the
 // launch device (bound from `out`).  lane_limit >= 0 (spo_eval_lanes): lanes
@@ -374,6 +383,17 @@ static int eval_impl(int kind, int dtype, int mode, const void *table, const int
                 g.cnt[ax] = (double)n3[ax];
                 g.delta[ax] = delta3[ax];
                 g.n[ax] = n3[ax];
+            }
+            // line-window kernel for batches dense enough to share stencil
+            // planes along grid lines (SPO_LINE=0/1 forces it off/on)
+            const char *env_line = getenv("SPO_LINE");
+            const long long cells = (long long)n3[0] * n3[1] * n3[2];
+            const bool line = env_line ? env_line[0] == '1' : n_pos * LINE_DENSITY_DEN >= cells * LINE_DENSITY_NUM;
+            if (line) {
+                const int r = eval_line(kind, dtype, table, geo, g, pos, n_pos, out, out_pos_stride,
+                                        out_stream_stride, reinterpret_cast<const long long *>(out_index), status,
+                                        workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream), lanes);
+                if (r >= 0) return r;
             }
             const int r = eval_tma(kind, dtype, table, geo, g, pos, n_pos, out, out_pos_stride, out_stream_stride,
                                    reinterpret_cast<const long long *>(out_index), status, workspace,

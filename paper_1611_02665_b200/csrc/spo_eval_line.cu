@@ -1,0 +1,561 @@
+// spo_eval_line.cu -- the line-window kernel: the FAST path for large batches
+// (fp32 and fp64).  Same per-orbital arithmetic as spo_eval_tma.cu (bitwise),
+// different data movement: stencil planes are shared between positions.
+//
+// Position p's 4x4x4 stencil is four planes i0..i0+3 of 4(j) x 4(k) rows.  Two
+// positions on the same grid line (j0, k0) with i0 values less than 4 apart
+// share planes.  So:
+//
+//  1. line_keys_kernel + cub radix sort + line_records_kernel: positions are
+//     sorted by (spatial block, j0, k0, i0) -- the 4x4x4 block order of
+//     spo_eval_tma.cu's bucketing for L2 locality, and inside a block whole
+//     lines in increasing i0 -- into records (36 weights, cell, original
+//     index).
+//  2. line_kernel: persistent CTAs (one per SM).  A work item is (unit u = a
+//     2 KB-wide slice of every table row: 512 fp32 / 256 fp64 lanes, run of up
+//     to BPL sorted positions), handed out by a global ticket in unit-major
+//     order.  One producer warp walks the run and loads each plane the run
+//     needs ONCE, in line order (plane = 16 rows x 2 KB = 32 KB as four
+//     512-byte-wide TMA boxes), into a 6-slot shared-memory ring; eight
+//     consumer warps (64 fp32 / 32 fp64 lanes each) evaluate every position of
+//     the run from the ring and release planes no later position needs
+//     (mbarrier full/empty pairs per slot).  With one position per cell along
+//     a line, a position needs ~1.2 new planes instead of 4: L2->SM traffic
+//     and the TMA shared-memory writes drop ~3x.
+//
+// The producer and the consumers derive the same plane sequence from the
+// records (plane_step below), so no plane ids are exchanged: plane number s
+// lives in slot s % R, phase s / R.
+#include <cuda.h>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include <cstdlib>
+
+#include "spo_common.cuh"
+#include "spo_prologue.cuh"
+#include "spo_tma.cuh"
+
+namespace spo {
+namespace line {
+
+using namespace tma;
+
+constexpr int ROWB = 512;                        // unit bytes per table row
+constexpr int BOXB = 512;                        // TMA box width in bytes
+static_assert(ROWB == BOXB, "one TMA box per plane");
+constexpr int BOX = 16 * BOXB;                   // bytes per box (16 rows)
+constexpr int PLANE = 16 * ROWB;                 // bytes per plane slot
+constexpr int BPL = 64;                          // positions per item
+constexpr int PL = 4 * BPL + 4;                  // plane-list ints per run: count, planes, pad
+constexpr int PLB = PL * 4;                      // plane-list bytes per run (16-byte multiple)
+constexpr int PBATCH = 4;                        // planes issued together by the producer lanes
+constexpr int WS_HEADER = 1024;                  // ticket @0
+constexpr int NBK = 4;                           // spatial blocks per axis (as spo_eval_tma.cu)
+constexpr int MAX_AXIS = 256;                    // cell index fits 8 bits of the sort key
+
+template <typename T>
+struct LT;
+// CONS consumer warps (+ one producer warp); consumer warp w evaluates the
+// positions q = w (mod CONS) of every run over the whole unit (one 16-byte
+// lane vector per thread: 4 fp32 / 2 fp64 orbitals)
+template <>
+struct LT<float> {
+    static constexpr int RECB = 36 * 4 + 16;
+    static constexpr int CONS = 11;  // + the producer: 12 warps, 3 per SMSP (13 would cap at 128 registers)
+    static constexpr int R = 24;     // plane slots
+};
+template <>
+struct LT<double> {
+    static constexpr int RECB = 36 * 8 + 16;
+    static constexpr int CONS = 7;   // fp64 weights need ~200 registers
+    static constexpr int R = 22;     // plane slots (larger records)
+};
+
+struct LArgs {
+    const unsigned char *recs;  // [n_pos][RECB], sorted
+    const int *plist;           // [runs][PL]: plane count, then i | j << 10 | k << 20 per plane
+    unsigned *ticket;
+    long long n_pos;
+    long long nbatch;           // ceil(n_pos / BPL)
+    long long n_items;          // units * nbatch
+    int nb;                     // table row length (lanes) per tile
+    void *out;
+    long long out_pos_stride, out_stream_stride;
+    const long long *out_index;
+    long long lane_limit;
+    int evict_last;
+};
+
+struct LItem {
+    long long b0;
+    int nb, u, valid, pad;
+};
+
+// ------------------------------------------------------------- prologue --
+__global__ void line_keys_kernel(GridArgs g, const double *__restrict__ pos, long long n, unsigned *__restrict__ keys,
+                                 int *__restrict__ vals, int *__restrict__ status) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x) {
+        double t;
+        const double x = pos[3 * p], y = pos[3 * p + 1], z = pos[3 * p + 2];
+        const int i0 = map_axis(x, g.dinv[0], g.cnt[0], &t);
+        const int j0 = map_axis(y, g.dinv[1], g.cnt[1], &t);
+        const int k0 = map_axis(z, g.dinv[2], g.cnt[2], &t);
+        unsigned key = 0xffffffffu;
+        if (isfinite(x) && isfinite(y) && isfinite(z)) {
+            const unsigned b = ((i0 * NBK / g.n[0]) * NBK + j0 * NBK / g.n[1]) * NBK + k0 * NBK / g.n[2];
+            key = (b << 24) | ((unsigned)j0 << 16) | ((unsigned)k0 << 8) | (unsigned)i0;
+        } else if (status) {
+            atomicOr(status, 1);
+        }
+        keys[p] = key;
+        vals[p] = (int)p;
+    }
+}
+
+template <typename T>
+__global__ void line_records_kernel(GridArgs g, const double *__restrict__ pos, const int *__restrict__ order,
+                                    long long n, unsigned char *__restrict__ recs) {
+    constexpr int RECB = LT<T>::RECB;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+         q += (long long)gridDim.x * blockDim.x) {
+        const long long p = order[q];
+        const double x = pos[3 * p], y = pos[3 * p + 1], z = pos[3 * p + 2];
+        double tx, ty, tz;
+        int i0 = map_axis(x, g.dinv[0], g.cnt[0], &tx);
+        const int j0 = map_axis(y, g.dinv[1], g.cnt[1], &ty);
+        const int k0 = map_axis(z, g.dinv[2], g.cnt[2], &tz);
+        T w[36];
+        axis_weights<T>(tx, g.dinv[0], g.delta[0], w);
+        axis_weights<T>(ty, g.dinv[1], g.delta[1], w + 12);
+        axis_weights<T>(tz, g.dinv[2], g.delta[2], w + 24);
+        if (!(isfinite(x) && isfinite(y) && isfinite(z))) i0 = -1;
+        unsigned char *dst = recs + q * RECB;
+#pragma unroll
+        for (int e = 0; e < 36 * (int)sizeof(T) / 16; ++e) {
+            float4 v;
+            memcpy(&v, reinterpret_cast<const unsigned char *>(w) + 16 * e, 16);
+            reinterpret_cast<float4 *>(dst)[e] = v;
+        }
+        *reinterpret_cast<int4 *>(dst + 36 * sizeof(T)) = make_int4(i0, j0 | (k0 << 16), 0, (int)p);
+    }
+}
+
+// ------------------------------------------------------- plane sequence --
+// The planes a run (BPL consecutive sorted positions) needs, numbered in load
+// order.  A position on the current line whose i0 lies inside the loaded
+// range reuses planes i0..last; new planes (max(last+1, i0) .. i0+3) get the
+// next numbers.  line_runs_kernel stores in every record the run-relative
+// number of its plane i0 (its planes are that number + 0..3) and in the
+// run's first record the run's plane count; the producer loads planes in
+// that order and the consumers find their planes by number: plane number s
+// lives in ring slot s % R, phase s / R.
+template <typename T>
+__global__ void line_runs_kernel(long long n, unsigned char *__restrict__ recs, int *__restrict__ plist) {
+    constexpr int RECB = LT<T>::RECB;
+    const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (b * BPL >= n) return;
+    const int nb = (int)min((long long)BPL, n - b * BPL);
+    unsigned char *rc = recs + b * BPL * RECB + 36 * sizeof(T);
+    int cj = -1, ck = -1, last = -1;
+    int next = 0;
+    for (int q = 0; q < nb; ++q) {
+        int4 *c = reinterpret_cast<int4 *>(rc + q * RECB);
+        const int4 cell = *c;
+        int s = 0;
+        if (cell.x >= 0) {
+            const int j0 = cell.y & 0xffff, k0 = cell.y >> 16, i0 = cell.x;
+            const bool same = j0 == cj && k0 == ck;
+            int lo;
+            if (same && i0 <= last) {
+                s = next - 1 - (last - i0);
+                lo = last + 1;
+            } else {
+                s = next;
+                lo = i0;
+            }
+            int *pl = plist + b * PL + 1;
+            for (int t = lo; t <= i0 + 3; ++t) pl[next++] = t | (j0 << 10) | (k0 << 20);
+            if (!same || i0 + 3 > last) last = i0 + 3;
+            cj = j0;
+            ck = k0;
+        }
+        c->z = s;
+    }
+    reinterpret_cast<int4 *>(rc)->z |= next << 16;
+    plist[b * PL] = next;
+}
+
+template <typename T>
+constexpr size_t smem_planes() {
+    return (size_t)LT<T>::R * PLANE;
+}
+template <typename T>
+constexpr size_t smem_bytes() {
+    return smem_planes<T>() + 2 * (size_t)BPL * LT<T>::RECB + 2 * (size_t)PLB + 2 * sizeof(LItem) +
+           (2 * LT<T>::R + 4) * 8;
+}
+static_assert(smem_bytes<float>() <= 232448, "shared memory budget");
+static_assert(smem_bytes<double>() <= 232448, "shared memory budget");
+
+// ---------------------------------------------------------------- kernel --
+template <int KIND, typename T>
+__global__ void __launch_bounds__((LT<T>::CONS + 1) * 32, 1) line_kernel(const __grid_constant__ CUtensorMap tmap, const LArgs a) {
+    constexpr int S = NS<KIND>::S;
+    constexpr int CONSUMERS = LT<T>::CONS;
+    constexpr int R = LT<T>::R;
+    constexpr int W = 16 / (int)sizeof(T);         // lanes per thread (16-byte vector)
+    constexpr int RECB = LT<T>::RECB;
+    constexpr int ULANES = ROWB / (int)sizeof(T);  // lanes per unit
+    constexpr int BOXL = BOXB / (int)sizeof(T);    // lanes per box = per consumer warp
+    static_assert(32 * W == BOXL, "a consumer warp covers one box");
+    using AV = typename Acc<T>::V;
+    constexpr int AN = Acc<T>::N;
+
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char *planes = smem;
+    unsigned char *recs = smem + smem_planes<T>();
+    int *plists = reinterpret_cast<int *>(recs + 2 * BPL * RECB);
+    LItem *info = reinterpret_cast<LItem *>(plists + 2 * PL);
+    unsigned long long *full = reinterpret_cast<unsigned long long *>(info + 2);
+    unsigned *relw = reinterpret_cast<unsigned *>(full + R);  // [CONSUMERS]: first plane each warp still needs
+    unsigned *issued = relw + CONSUMERS;                      // planes armed so far
+    unsigned long long *rfull = full + 2 * R;
+    unsigned long long *rempty = rfull + 2;
+    static_assert((CONSUMERS + 1) * 4 <= R * 8, "release words fit");
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x < CONSUMERS + 1) relw[threadIdx.x] = 0;  // and issued
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < R; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&rfull[s], 1);
+            mbar_init(&rempty[s], CONSUMERS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == CONSUMERS) {
+        // ------------------------------------------------------ producer --
+        // lane 0 takes tickets and loads run records + plane lists; lanes
+        // 0..PBATCH-1 issue the run's planes PBATCH at a time (one slot each)
+        const unsigned long long policy = l2_policy(a.evict_last);
+        auto fill = [&](int slot) {  // lane 0
+            const unsigned long long k = atomicAdd(a.ticket, 1u);
+            LItem it;
+            it.valid = k < (unsigned long long)a.n_items;
+            it.pad = 0;
+            if (it.valid) {
+                const long long u = (long long)k / a.nbatch;
+                const long long b = (long long)k - u * a.nbatch;
+                it.u = (int)u;
+                it.b0 = b * BPL;
+                it.nb = (int)min((long long)BPL, a.n_pos - it.b0);
+                info[slot] = it;
+                mbar_arrive_expect_tx(&rfull[slot], (unsigned)(it.nb * RECB + PLB));
+                bulk_load(recs + slot * BPL * RECB, a.recs + it.b0 * RECB, (unsigned)(it.nb * RECB), &rfull[slot]);
+                bulk_load(plists + slot * PL, a.plist + b * PL, (unsigned)PLB, &rfull[slot]);
+            } else {
+                it.u = it.nb = 0;
+                it.b0 = 0;
+                info[slot] = it;
+                mbar_arrive(&rfull[slot]);
+            }
+        };
+        // the records slot of item r-1 is refilled (item r+1) once the
+        // consumers release it: polled between plane batches
+        int pend = -1;
+        unsigned pend_par = 0;
+        auto poll = [&](bool block) {  // lane 0
+            if (pend < 0) return;
+            if (block)
+                mbar_wait(&rempty[pend], pend_par);
+            else if (!mbar_test(&rempty[pend], pend_par))
+                return;
+            fill(pend);
+            pend = -1;
+        };
+        if (lane == 0) {
+            fill(0);
+            fill(1);
+        }
+        __syncwarp();
+        unsigned base = 0;  // plane number of the current run's first plane
+        for (int r = 0;; ++r) {
+            const int slot = r & 1;
+            mbar_wait(&rfull[slot], (r >> 1) & 1);
+            const LItem it = info[slot];
+            if (!it.valid) break;
+            if (r >= 1) {
+                pend = slot ^ 1;  // item r-1's slot, for item r+1
+                pend_par = ((r - 1) >> 1) & 1;
+            }
+            const int *pl = plists + slot * PL;
+            const int count = pl[0];
+            const long long L = (long long)it.u * ULANES;  // the unit's first lane
+            const int tile = (int)(L / a.nb), lt = (int)(L - (long long)tile * a.nb);
+            for (int t0 = 0; t0 < count; t0 += PBATCH) {
+                const int nbt = min(PBATCH, count - t0);
+                const unsigned xlast = base + (unsigned)(t0 + nbt - 1);
+                if (xlast >= (unsigned)R) {
+                    // ring space: every consumer is done with the planes these slots held
+                    const unsigned need = xlast - R + 1;
+                    while (true) {
+                        unsigned v = lane < CONSUMERS ? ld_acquire_shared(&relw[lane]) : 0xffffffffu;
+                        v = __reduce_min_sync(0xffffffffu, v);
+                        if (v >= need) break;
+                    }
+                }
+                const int t = t0 + lane;
+                if (lane < nbt) {
+                    const unsigned s = base + (unsigned)t;
+                    const int sl = (int)(s % R);
+                    const unsigned n = s / R;
+                    // the slot's previous plane has landed (the producer observes
+                    // every plane in order, so the parity cannot alias)
+                    if (n > 0) mbar_wait(&full[sl], (n - 1) & 1);
+                    const int c = pl[1 + t];
+                    mbar_arrive_expect_tx(&full[sl], PLANE);
+                    tma_load_5d(planes + (size_t)sl * PLANE, &tmap, &full[sl], lt, (c >> 20) & 0x3ff,
+                                (c >> 10) & 0x3ff, c & 0x3ff, tile, policy);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    st_release_shared(issued, base + (unsigned)(t0 + nbt));
+                    poll(false);
+                }
+                __syncwarp();
+            }
+            base += (unsigned)count;
+            if (r >= 1 && lane == 0) poll(true);
+            __syncwarp();
+        }
+        return;
+    }
+
+    // -------------------------------------------------------- consumers --
+    // warp g evaluates positions q = g (mod CONSUMERS) of every run (the TMA
+    // kernel's contraction, one 16-byte lane vector per thread).  It waits
+    // only on its own planes: `issued` says a plane's slot is armed (so the
+    // parity wait is on the right phase), and relw[g] publishes the first
+    // plane it will need next (all below are free for the producer).
+    const int g = warp;
+    unsigned base = 0;
+    auto publish = [&](unsigned v) {
+        __syncwarp();
+        if (lane == 0) st_release_shared(&relw[g], v);
+    };
+    for (int r = 0;; ++r) {
+        const int slot = r & 1;
+        mbar_wait(&rfull[slot], (r >> 1) & 1);
+        const LItem it = info[slot];
+        if (!it.valid) break;
+        const unsigned char *rc = recs + slot * BPL * RECB;
+        const unsigned count = (unsigned)reinterpret_cast<const int4 *>(rc + 36 * sizeof(T))->z >> 16;
+        auto first_plane = [&](int q) -> unsigned {
+            if (q >= it.nb) return base + count;
+            const int4 c = *reinterpret_cast<const int4 *>(rc + q * RECB + 36 * sizeof(T));
+            return c.x < 0 ? base + count : base + (unsigned)(c.z & 0xffff);
+        };
+        publish(first_plane(g));
+        const long long L0 = (long long)it.u * ULANES + lane * W;  // output lane
+        const int nv = (int)max(0LL, min((long long)W, a.lane_limit - L0));
+        for (int q = g; q < it.nb; q += CONSUMERS) {
+            const unsigned char *rec = rc + q * RECB;
+            const int4 cell = *reinterpret_cast<const int4 *>(rec + 36 * sizeof(T));
+            const long long op = a.out_index ? a.out_index[cell.w] : cell.w;
+            T *o = reinterpret_cast<T *>(a.out) + op * a.out_pos_stride + L0;
+            AV acc[S][AN];
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int h = 0; h < AN; ++h) zero(acc[s][h]);
+            if (cell.x < 0) {
+                publish(first_plane(q + CONSUMERS));
+                if (nv == W)
+                    store_lane<S>(o, a.out_stream_stride, acc, false);
+                else if (nv > 0)
+                    store_lane_partial<S>(o, a.out_stream_stride, acc, false, nv);
+                continue;
+            }
+            const unsigned s0 = base + (unsigned)(cell.z & 0xffff);
+            const T *w = reinterpret_cast<const T *>(rec);
+            T wx[12], wy[12], wz[12];
+#pragma unroll
+            for (int e = 0; e < 12; ++e) {
+                wx[e] = w[e];
+                wy[e] = w[12 + e];
+                wz[e] = w[24 + e];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const unsigned x = s0 + (unsigned)i;
+                while (ld_acquire_shared(issued) <= x) {
+                }
+                const int sl = (int)(x % R);
+                mbar_wait(&full[sl], (x / R) & 1);
+                const T *p = reinterpret_cast<const T *>(planes + (size_t)sl * PLANE) + lane * W;
+                slab_contract<KIND, BOXL>(p, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
+            }
+            publish(first_plane(q + CONSUMERS));  // this position's planes are read
+            if (nv == W)
+                store_lane<S>(o, a.out_stream_stride, acc, true);
+            else if (nv > 0)
+                store_lane_partial<S>(o, a.out_stream_stride, acc, true, nv);
+        }
+        base += count;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rempty[slot]);
+    }
+}
+
+template <int KIND, typename T>
+static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
+    constexpr size_t sm = smem_bytes<T>();
+    int grid = (int)min((long long)sms, a.n_items);
+    if (grid < 1) grid = 1;
+    cudaFuncSetAttribute(line_kernel<KIND, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    line_kernel<KIND, T><<<grid, (LT<T>::CONS + 1) * 32, sm, st>>>(map, a);
+    return check_launch("spo_eval (line) launch");
+}
+
+static size_t pad256(size_t b) { return (b + 255) / 256 * 256; }
+
+}  // namespace line
+
+// Workspace of the line path: [header][keys in/out][order in/out][cub temp]
+// [records].  The radix-sort temp size is only known on a device; the bound
+// below covers it (checked at call time).
+static long long line_cub_bound(long long n) { return (4LL << 20) + (long long)line::pad256(4 * (size_t)n); }
+
+long long eval_line_workspace_bytes(int dtype, long long n_pos) {
+    using namespace line;
+    const long long recb = dtype == SPO_F64 ? LT<double>::RECB : LT<float>::RECB;
+    const long long runs = (n_pos + BPL - 1) / BPL;
+    return WS_HEADER + 4 * (long long)pad256(4 * n_pos) + line_cub_bound(n_pos) + (long long)pad256(n_pos * recb) +
+           runs * PLB;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn line_encode() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// Whether the line path can take this request (layout, grid, workspace).
+bool eval_line_eligible(int dtype, const TableGeom &geo, long long n_pos, long long ws_bytes) {
+    using namespace line;
+    const int E = dtype == SPO_F64 ? 8 : 4;
+    const long long row = (long long)geo.nb * E;
+    if (row % BOXB) return false;                                       // boxes must not straddle tiles
+    if (((long long)geo.nb * geo.n_tiles * E) % ROWB) return false;     // whole units
+    if (geo.nx > MAX_AXIS || geo.ny > MAX_AXIS || geo.nz > MAX_AXIS) return false;
+    if (n_pos >= (1LL << 31)) return false;
+    return ws_bytes >= eval_line_workspace_bytes(dtype, n_pos);
+}
+
+// Returns -1 when the request is not taken (the caller falls back).
+int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, const GridArgs &g, const double *pos,
+              long long n_pos, void *out, long long ops, long long oss, const long long *out_index, int *status,
+              void *workspace, long long ws_bytes, cudaStream_t st, long long lane_limit) {
+    using namespace line;
+    if (!eval_line_eligible(dtype, geo, n_pos, ws_bytes) || !aligned16(workspace)) return -1;
+    EncodeTiledFn encode = line_encode();
+    if (!encode) return -1;
+    const int E = dtype == SPO_F64 ? 8 : 4;
+    const int boxl = BOXB / E;
+
+    unsigned char *ws = static_cast<unsigned char *>(workspace);
+    const size_t vec = pad256(4 * (size_t)n_pos);
+    unsigned *keys_in = reinterpret_cast<unsigned *>(ws + WS_HEADER);
+    unsigned *keys_out = reinterpret_cast<unsigned *>(ws + WS_HEADER + vec);
+    int *vals_in = reinterpret_cast<int *>(ws + WS_HEADER + 2 * vec);
+    int *vals_out = reinterpret_cast<int *>(ws + WS_HEADER + 3 * vec);
+    unsigned char *temp = ws + WS_HEADER + 4 * vec;
+    size_t temp_bytes = 0;
+    if (cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)n_pos, 0, 32,
+                                        st) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    if ((long long)temp_bytes > line_cub_bound(n_pos)) return -1;
+    unsigned char *recs = temp + line_cub_bound(n_pos);
+    int *plist = reinterpret_cast<int *>(recs + pad256((size_t)n_pos * (dtype == SPO_F64 ? LT<double>::RECB
+                                                                                          : LT<float>::RECB)));
+
+    CUtensorMap map;
+    cuuint64_t dims[5] = {(cuuint64_t)geo.nb, (cuuint64_t)geo.nzp, (cuuint64_t)geo.nyp, (cuuint64_t)geo.nxp,
+                          (cuuint64_t)geo.n_tiles};
+    cuuint64_t strides[4] = {(cuuint64_t)geo.nb * E, (cuuint64_t)geo.nzp * geo.nb * E,
+                             (cuuint64_t)geo.nyp * geo.nzp * geo.nb * E, (cuuint64_t)geo.tile_stride * E};
+    cuuint32_t box[5] = {(cuuint32_t)boxl, 4, 4, 1, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = encode(&map, dtype == SPO_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5,
+                        const_cast<void *>(table), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+
+    if (cudaMemsetAsync(ws, 0, WS_HEADER, st) != cudaSuccess) return check_launch("workspace reset");
+    const long long blocks = min((n_pos + 255) / 256, 148LL * 16);
+    line_keys_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, keys_in, vals_in, status);
+    if (cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)n_pos, 0, 32,
+                                        st) != cudaSuccess)
+        return check_launch("spo_eval (line sort)");
+    const unsigned run_blocks = (unsigned)((n_pos + (long long)BPL * 128 - 1) / ((long long)BPL * 128));
+    if (dtype == SPO_F64) {
+        line_records_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(g, pos, vals_out, n_pos, recs);
+        line_runs_kernel<double><<<run_blocks, 128, 0, st>>>(n_pos, recs, plist);
+    } else {
+        line_records_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(g, pos, vals_out, n_pos, recs);
+        line_runs_kernel<float><<<run_blocks, 128, 0, st>>>(n_pos, recs, plist);
+    }
+    int rc = check_launch("spo_eval (line prologue)");
+    if (rc) return rc;
+
+    LArgs a;
+    a.recs = recs;
+    a.plist = plist;
+    a.ticket = reinterpret_cast<unsigned *>(ws);
+    a.n_pos = n_pos;
+    a.nbatch = (n_pos + BPL - 1) / BPL;
+    const long long units = (long long)geo.nb * geo.n_tiles * E / ROWB;
+    a.n_items = a.nbatch * units;
+    if (a.n_items >= (1LL << 32)) return -1;
+    a.nb = geo.nb;
+    a.out = out;
+    a.out_pos_stride = ops;
+    a.out_stream_stride = oss;
+    a.out_index = out_index;
+    a.lane_limit = lane_limit;
+    static const char *env_hint = getenv("SPO_L2HINT");
+    a.evict_last = !(env_hint && env_hint[0] == '0');
+
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (dtype == SPO_F64) {
+        if (kind == SPO_KIND_V) return launch<SPO_KIND_V, double>(map, a, sms, st);
+        if (kind == SPO_KIND_VGL) return launch<SPO_KIND_VGL, double>(map, a, sms, st);
+        return launch<SPO_KIND_VGH, double>(map, a, sms, st);
+    }
+    if (kind == SPO_KIND_V) return launch<SPO_KIND_V, float>(map, a, sms, st);
+    if (kind == SPO_KIND_VGL) return launch<SPO_KIND_VGL, float>(map, a, sms, st);
+    return launch<SPO_KIND_VGH, float>(map, a, sms, st);
+}
+
+}  // namespace spo

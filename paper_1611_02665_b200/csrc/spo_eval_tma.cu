@@ -30,6 +30,7 @@
 
 #include "spo_common.cuh"
 #include "spo_prologue.cuh"
+#include "spo_tma.cuh"
 
 namespace spo {
 namespace tma {
@@ -81,243 +82,6 @@ struct Args {
     long long coef_stride;
     double *partials;           // [units][n_pos][S]
 };
-
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, unsigned long long *bar, int c0,
-                                            int c1, int c2, int c3, int c4, unsigned long long policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<unsigned long long>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
-        "r"(c4), "l"(policy)
-        : "memory");
-}
-
-// L2 policy for table slabs: keep the current unit's slice resident while the
-// output stream (st.global.cs) passes through.
-__device__ __forceinline__ unsigned long long l2_policy(bool evict_last) {
-    unsigned long long p;
-    if (evict_last)
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    else
-        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-
-__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<unsigned long long>(src)), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-template <int KIND>
-struct NS {
-    static constexpr int S = KIND == SPO_KIND_V ? 1 : (KIND == SPO_KIND_VGL ? 5 : 10);
-};
-
-// ----------------------------------------------------------- contraction --
-// Packed fp32x2 FMA (SASS FFMA2, sm_100): two independent round-to-nearest
-// fp32 FMAs per instruction with a broadcast scalar multiplier -- bitwise the
-// same as two __fmaf_rn, at half the issue slots.
-__device__ __forceinline__ float2 fma2(float w, float2 c, float2 acc) {
-    return __ffma2_rn(make_float2(w, w), c, acc);
-}
-__device__ __forceinline__ float2 mul2(float w, float2 c) { return __fmul2_rn(make_float2(w, w), c); }
-
-// One i-slab for one lane: 4 fp32 orbitals as two fp32x2 pairs.
-// slab: [j][k][CW] of this lane's position; wy/wz: 12 weights; ax/dax/d2ax: x weights of this i.
-template <int KIND, int CW>
-__device__ __forceinline__ void slab_contract(const float *__restrict__ slab, const float (&wy)[12],
-                                              const float (&wz)[12], float ax, float dax, float d2ax,
-                                              float2 (&acc)[NS<KIND>::S][2]) {
-    float2 t00[2], t10[2], t01[2], t20[2], t11[2], t02[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) t00[h] = t10[h] = t01[h] = t20[h] = t11[h] = t02[h] = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        float4 c[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const float4 *>(slab + (j * 4 + k) * CW);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const float2 c0 = h ? make_float2(c[0].z, c[0].w) : make_float2(c[0].x, c[0].y);
-            const float2 c1 = h ? make_float2(c[1].z, c[1].w) : make_float2(c[1].x, c[1].y);
-            const float2 c2 = h ? make_float2(c[2].z, c[2].w) : make_float2(c[2].x, c[2].y);
-            const float2 c3 = h ? make_float2(c[3].z, c[3].w) : make_float2(c[3].x, c[3].y);
-            const float2 s0 = fma2(wz[3], c3, fma2(wz[2], c2, fma2(wz[1], c1, mul2(wz[0], c0))));
-            t00[h] = fma2(wy[j], s0, t00[h]);
-            if (KIND != SPO_KIND_V) {
-                const float2 s1 = fma2(wz[7], c3, fma2(wz[6], c2, fma2(wz[5], c1, mul2(wz[4], c0))));
-                const float2 s2 = fma2(wz[11], c3, fma2(wz[10], c2, fma2(wz[9], c1, mul2(wz[8], c0))));
-                t10[h] = fma2(wy[4 + j], s0, t10[h]);
-                t01[h] = fma2(wy[j], s1, t01[h]);
-                t20[h] = fma2(wy[8 + j], s0, t20[h]);
-                t02[h] = fma2(wy[j], s2, t02[h]);
-                if (KIND == SPO_KIND_VGH) t11[h] = fma2(wy[4 + j], s1, t11[h]);
-            }
-        }
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        acc[0][h] = fma2(ax, t00[h], acc[0][h]);
-        if (KIND != SPO_KIND_V) {
-            acc[1][h] = fma2(dax, t00[h], acc[1][h]);
-            acc[2][h] = fma2(ax, t10[h], acc[2][h]);
-            acc[3][h] = fma2(ax, t01[h], acc[3][h]);
-        }
-        if (KIND == SPO_KIND_VGL) acc[4][h] = fma2(d2ax, t00[h], fma2(ax, t20[h], fma2(ax, t02[h], acc[4][h])));
-        if (KIND == SPO_KIND_VGH) {
-            acc[4][h] = fma2(d2ax, t00[h], acc[4][h]);
-            acc[5][h] = fma2(dax, t10[h], acc[5][h]);
-            acc[6][h] = fma2(dax, t01[h], acc[6][h]);
-            acc[7][h] = fma2(ax, t20[h], acc[7][h]);
-            acc[8][h] = fma2(ax, t11[h], acc[8][h]);
-            acc[9][h] = fma2(ax, t02[h], acc[9][h]);
-        }
-    }
-}
-
-// One i-slab for one lane: 2 fp64 orbitals, DFMA in the generic kernel's order.
-template <int KIND, int CW>
-__device__ __forceinline__ void slab_contract(const double *__restrict__ slab, const double (&wy)[12],
-                                              const double (&wz)[12], double ax, double dax, double d2ax,
-                                              double2 (&acc)[NS<KIND>::S][1]) {
-    double t00[2], t10[2], t01[2], t20[2], t11[2], t02[2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) t00[e] = t10[e] = t01[e] = t20[e] = t11[e] = t02[e] = 0.0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        double2 c[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const double2 *>(slab + (j * 4 + k) * CW);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const double c0 = e ? c[0].y : c[0].x, c1 = e ? c[1].y : c[1].x;
-            const double c2 = e ? c[2].y : c[2].x, c3 = e ? c[3].y : c[3].x;
-            const double s0 = __fma_rn(wz[3], c3, __fma_rn(wz[2], c2, __fma_rn(wz[1], c1, wz[0] * c0)));
-            t00[e] = __fma_rn(wy[j], s0, t00[e]);
-            if (KIND != SPO_KIND_V) {
-                const double s1 = __fma_rn(wz[7], c3, __fma_rn(wz[6], c2, __fma_rn(wz[5], c1, wz[4] * c0)));
-                const double s2 = __fma_rn(wz[11], c3, __fma_rn(wz[10], c2, __fma_rn(wz[9], c1, wz[8] * c0)));
-                t10[e] = __fma_rn(wy[4 + j], s0, t10[e]);
-                t01[e] = __fma_rn(wy[j], s1, t01[e]);
-                t20[e] = __fma_rn(wy[8 + j], s0, t20[e]);
-                t02[e] = __fma_rn(wy[j], s2, t02[e]);
-                if (KIND == SPO_KIND_VGH) t11[e] = __fma_rn(wy[4 + j], s1, t11[e]);
-            }
-        }
-    }
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        double *a0 = e ? &acc[0][0].y : &acc[0][0].x;
-        *a0 = __fma_rn(ax, t00[e], *a0);
-        if (KIND != SPO_KIND_V) {
-            double *a1 = e ? &acc[1][0].y : &acc[1][0].x;
-            double *a2 = e ? &acc[2][0].y : &acc[2][0].x;
-            double *a3 = e ? &acc[3][0].y : &acc[3][0].x;
-            *a1 = __fma_rn(dax, t00[e], *a1);
-            *a2 = __fma_rn(ax, t10[e], *a2);
-            *a3 = __fma_rn(ax, t01[e], *a3);
-        }
-        if (KIND == SPO_KIND_VGL) {
-            double *a4 = e ? &acc[4][0].y : &acc[4][0].x;
-            *a4 = __fma_rn(d2ax, t00[e], __fma_rn(ax, t20[e], __fma_rn(ax, t02[e], *a4)));
-        }
-        if (KIND == SPO_KIND_VGH) {
-            double *a4 = e ? &acc[4][0].y : &acc[4][0].x;
-            double *a5 = e ? &acc[5][0].y : &acc[5][0].x;
-            double *a6 = e ? &acc[6][0].y : &acc[6][0].x;
-            double *a7 = e ? &acc[7][0].y : &acc[7][0].x;
-            double *a8 = e ? &acc[8][0].y : &acc[8][0].x;
-            double *a9 = e ? &acc[9][0].y : &acc[9][0].x;
-            *a4 = __fma_rn(d2ax, t00[e], *a4);
-            *a5 = __fma_rn(dax, t10[e], *a5);
-            *a6 = __fma_rn(dax, t01[e], *a6);
-            *a7 = __fma_rn(ax, t20[e], *a7);
-            *a8 = __fma_rn(ax, t11[e], *a8);
-            *a9 = __fma_rn(ax, t02[e], *a9);
-        }
-    }
-}
-
-template <typename T>
-struct Acc;
-template <>
-struct Acc<float> {
-    using V = float2;
-    static constexpr int N = 2;  // two fp32x2 pairs = the lane's 4 orbitals
-};
-template <>
-struct Acc<double> {
-    using V = double2;
-    static constexpr int N = 1;  // one pair = the lane's 2 orbitals
-};
-
-__device__ __forceinline__ void zero(float2 &v) { v = make_float2(0.f, 0.f); }
-__device__ __forceinline__ void zero(double2 &v) { v = make_double2(0.0, 0.0); }
-
-template <int S>
-__device__ __forceinline__ void store_lane(float *o, long long sstride, const float2 (&acc)[S][2], bool finite) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-        const float4 v = finite ? make_float4(acc[s][0].x, acc[s][0].y, acc[s][1].x, acc[s][1].y)
-                                : make_float4(NAN, NAN, NAN, NAN);
-        __stcs(reinterpret_cast<float4 *>(o + s * sstride), v);
-    }
-}
-template <int S>
-__device__ __forceinline__ void store_lane(double *o, long long sstride, const double2 (&acc)[S][1], bool finite) {
-#pragma unroll
-    for (int s = 0; s < S; ++s)
-        __stcs(reinterpret_cast<double2 *>(o + s * sstride), finite ? acc[s][0] : make_double2(NAN, NAN));
-}
-// the lane vector straddles lane_limit: store its first `nv` lanes only
-// (unrolled + predicated: no dynamic indexing of the accumulators)
-template <int S>
-__device__ __forceinline__ void store_lane_partial(float *o, long long sstride, const float2 (&acc)[S][2],
-                                                   bool finite, int nv) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-        if (nv > 0) o[s * sstride + 0] = finite ? acc[s][0].x : NAN;
-        if (nv > 1) o[s * sstride + 1] = finite ? acc[s][0].y : NAN;
-        if (nv > 2) o[s * sstride + 2] = finite ? acc[s][1].x : NAN;
-    }
-}
-template <int S>
-__device__ __forceinline__ void store_lane_partial(double *o, long long sstride, const double2 (&acc)[S][1],
-                                                   bool finite, int nv) {
-#pragma unroll
-    for (int s = 0; s < S; ++s)
-        if (nv > 0) o[s * sstride] = finite ? acc[s][0].x : NAN;
-}
 
 // ------------------------------------------------------------ prologue --
 // Positions are binned by the spatial block (NBK^3 blocks of the grid) of

@@ -392,7 +392,7 @@ def _as_positions(pos, check_finite: bool = True) -> np.ndarray:
 
 # Drop-in path: positions per device pass, and the scratch bytes it may use.
 DROPIN_CHUNK = 1 << 18
-DROPIN_SCRATCH_BYTES = 16 << 30
+DROPIN_SCRATCH_BYTES = 48 << 30
 # Batches larger than this are checked for non-finite positions on the device
 # (the kernels' status flag) instead of by a host pass; either way DomainError
 # is raised before the caller's buffers are touched.

@@ -1,0 +1,126 @@
+"""The line-window kernel (spo_eval_line.cu: stencil planes shared along grid
+lines) is bitwise identical to the per-position TMA kernel and the generic
+kernel on every input class: kinds, fp32/fp64, tiled/untiled tables, ragged
+runs, duplicate cells, a single line, non-finite positions, out_index,
+lane_limit, and grids too large for its sort key (fallback).  SPO_LINE=1/0
+forces the path (read on every call)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1611_02665_b200 import DeviceTable, DomainError, KernelKind, evaluate, streams
+from paper_1611_02665_b200.grid import GridSpec, unit_cell_grid
+
+pytestmark = pytest.mark.gpu
+
+
+def _both(monkeypatch, dt, kind, pos, **kw):
+    monkeypatch.setenv("SPO_LINE", "1")
+    a = evaluate(dt, kind, pos, pipeline=True, **kw).clone()
+    monkeypatch.setenv("SPO_LINE", "0")
+    b = evaluate(dt, kind, pos, pipeline=True, **kw)
+    monkeypatch.delenv("SPO_LINE")
+    return a, b
+
+
+def _eq(a, b):
+    import torch
+
+    return bool(torch.equal(a.nan_to_num(123.0), b.nan_to_num(123.0)))
+
+
+@pytest.mark.parametrize("kind", ["v", "vgl", "vgh"])
+@pytest.mark.parametrize("tile", ["auto", None])
+def test_line_bitwise_fp32(monkeypatch, kind, tile):
+    dt = DeviceTable.random(unit_cell_grid(20), 512, seed=5, tile_size=tile)
+    pos = np.random.default_rng(2).random((30000 + 17, 3)) * 3.0 - 1.0  # ragged last run, wrapped inputs
+    a, b = _both(monkeypatch, dt, kind, pos)
+    assert _eq(a, b)
+
+
+@pytest.mark.parametrize("kind", ["v", "vgh"])
+def test_line_bitwise_fp64(monkeypatch, kind):
+    dt = DeviceTable.normal_f64(unit_cell_grid(16), 128, seed=5)
+    pos = np.random.default_rng(3).random((20000, 3))
+    a, b = _both(monkeypatch, dt, kind, pos)
+    assert _eq(a, b)
+
+
+def test_line_matches_oracle(monkeypatch):
+    """Anchor: the line path against the fp64 oracle at 1e-5 * sum|w*c|."""
+    grid = unit_cell_grid(12)
+    dt = DeviceTable.random(grid, 256, seed=9)
+    pos = np.random.default_rng(4).random((4000, 3))
+    monkeypatch.setenv("SPO_LINE", "1")
+    got = streams(evaluate(dt, "vgh", pos, pipeline=True), dt, "vgh")
+    names = KernelKind("vgh").stream_names
+    sample = np.arange(0, 4000, 37)
+    ref, scale = oracle.eval_f64("vgh", dt.reference_soa(), 256, grid.spacings, pos[sample])
+    g = np.stack([got[n].cpu().numpy()[sample] for n in names], axis=1)
+    ok, worst = oracle.tolerance_check(g, ref, scale, 1e-5)
+    assert ok, worst
+
+
+def test_line_duplicate_cells_and_single_line(monkeypatch):
+    rng = np.random.default_rng(5)
+    dt = DeviceTable.random(unit_cell_grid(24), 256, seed=1)
+    # 40 cells, ~250 positions each: runs made of repeated cells
+    centers = rng.integers(0, 24, size=(40, 3)) / 24.0
+    dup = centers[rng.integers(0, 40, size=10000)] + rng.random((10000, 3)) * (0.9 / 24)
+    a, b = _both(monkeypatch, dt, "vgh", dup)
+    assert _eq(a, b)
+    # every position on one grid line (fixed y, z): maximal plane sharing
+    line = np.stack([rng.random(8000) * 2 - 0.5, np.full(8000, 0.31), np.full(8000, 0.77)], axis=1)
+    a, b = _both(monkeypatch, dt, "vgl", line)
+    assert _eq(a, b)
+
+
+def test_line_nonfinite_positions(monkeypatch):
+    import torch
+
+    dt = DeviceTable.random(unit_cell_grid(16), 128, seed=2)
+    pos = np.random.default_rng(6).random((5000, 3))
+    pos[[3, 777, 4999], [0, 1, 2]] = [np.nan, np.inf, -np.inf]
+    pos = torch.from_numpy(pos).cuda()  # device input: checked by the kernels' status flag
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    a, b = _both(monkeypatch, dt, "vgh", pos, status=st, check=False)
+    assert _eq(a, b) and int(st.item()) == 1
+    assert bool(torch.isnan(a[777]).all()) and not bool(torch.isnan(a[778]).any())
+    monkeypatch.setenv("SPO_LINE", "1")
+    with pytest.raises(DomainError):
+        evaluate(dt, "vgh", pos, pipeline=True)
+
+
+def test_line_out_index_and_lane_limit(monkeypatch):
+    import torch
+
+    dt = DeviceTable.random(unit_cell_grid(16), 256, seed=3)
+    P = 6000
+    pos = np.random.default_rng(7).random((P, 3))
+    perm = torch.from_numpy(np.random.default_rng(8).permutation(P)).cuda()
+    outs = []
+    for v in ("1", "0"):
+        monkeypatch.setenv("SPO_LINE", v)
+        o = torch.full((P, 10, dt.lanes), 5.0, device="cuda")
+        evaluate(dt, "vgh", pos, o, out_index=perm, pipeline=True)
+        buf = torch.full((P, 10, 300), 5.0, device="cuda")
+        evaluate(dt, "vgh", pos, buf[:, :, 4:], pipeline=True, lane_limit=201)
+        outs.append((o, buf))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    assert bool((outs[0][1][:, :, 205:] == 5.0).all())
+
+
+def test_line_wide_and_ragged_tiles(monkeypatch):
+    dt = DeviceTable.random(unit_cell_grid(12), 1000, seed=4)  # last tile partially filled
+    pos = np.random.default_rng(9).random((7000, 3))
+    a, b = _both(monkeypatch, dt, "vgh", pos)
+    assert _eq(a, b)
+
+
+def test_line_large_grid_falls_back(monkeypatch):
+    """Axes above 256 cells do not fit the sort key: the TMA kernel runs."""
+    grid = GridSpec(300, 4, 4, 1 / 300, 0.25, 0.25)
+    dt = DeviceTable.random(grid, 32, seed=1)
+    pos = np.random.default_rng(1).random((9000, 3))
+    a, b = _both(monkeypatch, dt, "v", pos)
+    assert _eq(a, b)
