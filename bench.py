@@ -322,18 +322,21 @@ def run_b200(args):
     total_units = P * N * args.steps * world
     value = total_units / (elapsed_ms / 1e3)
 
-    from paper_1611_02665_b200 import _abi
+    from paper_1611_02665_b200.kernels import eval_path
 
-    pipelined = args.mode == "fast" and _abi.load().spo_eval_workspace_bytes(
-        KernelKind(kind).code, 0, 0, chunk) > 0
-    # bucket_count_kernel + prologue_records_kernel + eval_tma_kernel
-    kernels_per_call = 3 if pipelined else 1
-    kernel_name = (f"spo::tma::eval_tma_kernel<{kind.upper()}> (+ prologue_records_kernel, timed together)"
-                   if pipelined else f"spo::eval_kernel<{kind.upper()},float,{args.mode}>")
+    path = eval_path(table, kind, chunk, mode=args.mode)
+    # this repo's kernels per evaluate() call (library kernels -- cub's radix
+    # sort in the line path's prologue, memsets -- not counted)
+    kernels_per_call, kernel_name = {
+        "line": (4, f"spo::line::line_kernel<{kind.upper()},float> (+ line_keys, cub sort, line_records, "
+                    f"line_runs prologue, timed together)"),
+        "tma": (3, f"spo::tma::eval_tma_kernel<{kind.upper()}> (+ bucket_count, prologue_records, timed together)"),
+        "generic": (1, f"spo::eval_kernel<{kind.upper()},float,{args.mode}>"),
+    }[path]
     peak, peak_src = measured_peak()
     achieved = bpp * chunk / (avg_launch_ms * 1e-3) / 1e9  # GB/s per launch
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(args, cfg, kind, chunk),
+                "frac": achieved / peak, "traffic": ncu_traffic(args, cfg, kind, chunk, path),
                 "peak_source": peak_src, "kernel": kernel_name,
                 "algorithmic_bytes_per_position": bpp, "positions_per_launch": chunk,
                 "avg_launch_ms": avg_launch_ms}
@@ -347,7 +350,7 @@ def run_b200(args):
                 "reference numpy fill), reference Philox walker position streams (seed 1)",
         "config": {"workload": f"cfg{cfg.index}: {cfg.description}", "grid": list(cfg.grid.counts),
                    "n_splines": N, "kernel": kind, "positions_per_gpu": P, "walkers_per_gpu": P // cfg.moves,
-                   "chunk": chunk, "mode": args.mode, "tile_size": table.tile_size,
+                   "chunk": chunk, "mode": args.mode, "path": path, "tile_size": table.tile_size,
                    "table_gb": table.nbytes / 1e9,
                    "l2": f"inputs larger than L2 (table {table.nbytes / 1e9:.2f} GB >> 126 MB); no flush",
                    "parallelism": f"walker-sharded x{world}, table replicated"},
@@ -439,13 +442,13 @@ def e2e_dropin(table, kind, pos_np, N, S, eval_batch, WalkerOutputsSoA, args, de
             "api": "paper_1611_02665_b200.eval_batch(table, kind, host positions, host WalkerOutputsSoA)"}
 
 
-def ncu_traffic(args, cfg, kind, chunk):
+def ncu_traffic(args, cfg, kind, chunk, path):
     """dram read+write bytes per launch from the committed ncu capture, when
     it was taken on this exact configuration (profiles/ncu_traffic.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             rec = json.load(f)
-        key = f"cfg{cfg.index}-{kind}-{args.mode}-tile{args.tile}"
+        key = f"cfg{cfg.index}-{kind}-{args.mode}-tile{args.tile}-{path}"
         r = rec.get(key)
         if r and r.get("positions_per_launch") == chunk:
             return r["dram_bytes_per_launch"]

@@ -60,7 +60,7 @@
 extern "C" {
 #endif
 
-#define SPO_ABI_VERSION 4
+#define SPO_ABI_VERSION 5
 
 /* kernel kinds: KernelKind (kernels.py:26-51) */
 #define SPO_KIND_V 0
@@ -126,6 +126,20 @@ int spo_eval_lanes(int kind, int dtype, int mode, const void *table, const int32
                    int64_t workspace_bytes, void *stream);
 
 /* Workspace spo_eval wants for this request (0 = none used, -1 = bad args). */
+/*
+ * Which kernel spo_eval runs for this request (no launch, no device needed):
+ *   SPO_PATH_GENERIC  one-pass kernel (strict mode, no workspace, small batches)
+ *   SPO_PATH_TMA      per-position TMA pipeline (spo_eval_tma.cu)
+ *   SPO_PATH_LINE     line-window kernel: planes shared along grid lines, for
+ *                     batches of >= 0.5 positions per grid cell (spo_eval_line.cu)
+ * -1 on bad arguments.  All paths give bitwise identical results.
+ */
+#define SPO_PATH_GENERIC 0
+#define SPO_PATH_TMA 1
+#define SPO_PATH_LINE 2
+int spo_eval_path(int kind, int dtype, int mode, const int32_t *n3, int32_t nb, int32_t n_tiles, int64_t n_pos,
+                  int64_t workspace_bytes);
+
 int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64_t n_pos);
 
 /*

@@ -18,9 +18,10 @@ LIB_PATH = os.path.join(_PKG, "libspo_b200.so")
 KIND_V, KIND_VGL, KIND_VGH = 0, 1, 2
 F32, F64 = 0, 1
 MODE_FAST, MODE_STRICT = 0, 1
-ABI_VERSION = 4
+ABI_VERSION = 5
 
-EXPORTS = ("spo_abi_version", "spo_last_error", "spo_eval", "spo_eval_lanes", "spo_eval_workspace_bytes",
+EXPORTS = ("spo_abi_version", "spo_last_error", "spo_eval", "spo_eval_lanes", "spo_eval_path",
+           "spo_eval_workspace_bytes",
            "spo_eval_ratios", "spo_eval_ratios_workspace_bytes", "spo_prologue",
            "spo_basis_weights",
            "spo_pack_table",
@@ -58,6 +59,8 @@ def load(build_if_missing: bool = True):
         L.spo_eval_lanes.restype = ip
         L.spo_eval_lanes.argtypes = [ip, ip, ip, vp, P(i32), i32, i32, P(dbl), P(dbl), vp, i64, vp, i64,
                                      i64, i64, vp, vp, vp, i64, vp]
+        L.spo_eval_path.restype = ip
+        L.spo_eval_path.argtypes = [ip, ip, ip, P(i32), i32, i32, i64, i64]
         L.spo_eval_workspace_bytes.restype = i64
         L.spo_eval_workspace_bytes.argtypes = [ip, ip, ip, i64]
         L.spo_eval_ratios_workspace_bytes.restype = i64

@@ -302,6 +302,7 @@ int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const
              const void *coef = nullptr, long long coef_stride = 0, double *ratios = nullptr);
 long long eval_tma_workspace_bytes(int dtype, long long n_pos);
 long long eval_line_workspace_bytes(int dtype, long long n_pos);
+bool eval_line_eligible(int dtype, const TableGeom &geo, long long n_pos, long long ws_bytes);
 int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, const GridArgs &g, const double *pos,
               long long n_pos, void *out, long long ops, long long oss, const long long *out_index, int *status,
               void *workspace, long long ws_bytes, cudaStream_t st, long long lane_limit);
@@ -324,6 +325,15 @@ extern "C" int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64
 // positions per grid cell from which the line-window kernel is used (NUM/DEN):
 // sustained-rate crossover measured by scripts/micro/line_sustained.py
 constexpr long long LINE_DENSITY_NUM = 1, LINE_DENSITY_DEN = 2;
+
+// line-window kernel for batches dense enough to share stencil planes along
+// grid lines (SPO_LINE=0/1 forces it off/on; read on every call)
+static bool want_line(const int32_t *n3, long long n_pos) {
+    const char *env_line = getenv("SPO_LINE");
+    if (env_line) return env_line[0] == '1';
+    const long long cells = (long long)n3[0] * n3[1] * n3[2];
+    return n_pos * LINE_DENSITY_DEN >= cells * LINE_DENSITY_NUM;
+}
 
 // lane_limit < 0: every table lane is stored and `out` must be memory of the
 // launch device (bound from `out`).  lane_limit >= 0 (spo_eval_lanes): lanes
@@ -384,12 +394,7 @@ static int eval_impl(int kind, int dtype, int mode, const void *table, const int
                 g.delta[ax] = delta3[ax];
                 g.n[ax] = n3[ax];
             }
-            // line-window kernel for batches dense enough to share stencil
-            // planes along grid lines (SPO_LINE=0/1 forces it off/on)
-            const char *env_line = getenv("SPO_LINE");
-            const long long cells = (long long)n3[0] * n3[1] * n3[2];
-            const bool line = env_line ? env_line[0] == '1' : n_pos * LINE_DENSITY_DEN >= cells * LINE_DENSITY_NUM;
-            if (line) {
+            if (want_line(n3, n_pos)) {
                 const int r = eval_line(kind, dtype, table, geo, g, pos, n_pos, out, out_pos_stride,
                                         out_stream_stride, reinterpret_cast<const long long *>(out_index), status,
                                         workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream), lanes);
@@ -467,6 +472,19 @@ static int eval_impl(int kind, int dtype, int mode, const void *table, const int
         case SPO_KIND_VGL: return launch<SPO_KIND_VGL, float, false>(a, grid, block, smem, st);
         default: return launch<SPO_KIND_VGH, float, false>(a, grid, block, smem, st);
     }
+}
+
+extern "C" int spo_eval_path(int kind, int dtype, int mode, const int32_t *n3, int32_t nb, int32_t n_tiles,
+                             int64_t n_pos, int64_t workspace_bytes) {
+    if (kind < SPO_KIND_V || kind > SPO_KIND_VGH || (dtype != SPO_F32 && dtype != SPO_F64) || n_pos < 0) return -1;
+    TableGeom geo;
+    if (make_geom(n3, nb, n_tiles, dtype, &geo)) return -1;
+    if (mode != SPO_MODE_FAST || workspace_bytes <= 0) return SPO_PATH_GENERIC;
+    const char *env_tma = getenv("SPO_TMA");
+    if (env_tma && env_tma[0] == '0') return SPO_PATH_GENERIC;
+    if (want_line(n3, n_pos) && eval_line_eligible(dtype, geo, n_pos, workspace_bytes)) return SPO_PATH_LINE;
+    if (workspace_bytes >= eval_tma_workspace_bytes(dtype, n_pos) && n_pos < (1LL << 31)) return SPO_PATH_TMA;
+    return SPO_PATH_GENERIC;
 }
 
 extern "C" int spo_eval(int kind, int dtype, int mode, const void *table, const int32_t *n3,

@@ -281,6 +281,27 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
     return out
 
 
+_PATHS = {0: "generic", 1: "tma", 2: "line"}
+
+
+def eval_path(table, kind, n_positions: int, *, mode: str = "fast", pipeline="auto") -> str:
+    """The kernel evaluate() runs for this request: "generic" (one pass),
+    "tma" (per-position TMA pipeline) or "line" (planes shared along grid
+    lines) -- spo_eval_path; all give bitwise identical results."""
+    kind = as_kind(kind)
+    dt = as_device_table(table)
+    L = _abi.load()
+    P = int(n_positions)
+    if pipeline == "auto":
+        pipeline = P * dt.lanes >= PIPELINE_MIN_WORK
+    ws = int(L.spo_eval_workspace_bytes(kind.code, dt.dtype_code, _MODES[mode], P)) if pipeline else 0
+    code = L.spo_eval_path(kind.code, dt.dtype_code, _MODES[mode], _abi.i32x3(dt.grid.counts), dt.nb,
+                           dt.n_tiles, P, max(ws, 0))
+    if code < 0:
+        raise ContractError("bad evaluation request")
+    return _PATHS[code]
+
+
 def evaluate_v(table, positions, out=None, **kw):
     return evaluate(table, KernelKind.V, positions, out, **kw)
 

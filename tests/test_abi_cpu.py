@@ -34,7 +34,7 @@ def test_library_exports_every_header_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.spo_abi_version() == 4
+    assert lib.spo_abi_version() == 5
     assert lib.spo_eval_ratios_workspace_bytes(2, 0, 128, 32, 1000) > 1000 * 160 + 32 * 1000 * 10 * 8 - 1
     assert lib.spo_eval_ratios_workspace_bytes(2, 0, 96, 1, 1000) == -1  # 384-byte rows
     assert lib.spo_eval_workspace_bytes(2, 0, 0, 1000) >= 1000 * 160
@@ -84,6 +84,24 @@ def test_eval_lanes_argument_validation(lib):
     assert _eval_lanes(lib, 20, ss=20, ps=200, n=0) == 0  # empty batch: no-op
     assert _eval_lanes(lib, 20, ss=22) == 1         # strides must be multiples of 4 lanes
     assert b"multiples" in lib.spo_last_error()
+
+
+def test_eval_path_selection(lib, monkeypatch):
+    """spo_eval_path: the kernel spo_eval would run (no device needed)."""
+    monkeypatch.delenv("SPO_LINE", raising=False)
+    n3 = _abi.i32x3((64, 64, 64))
+    big = 1 << 40
+    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, big) == 2    # >= 0.5 positions per cell: line
+    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 100000, big) == 1    # sparser: per-position TMA
+    assert lib.spo_eval_path(2, 0, 1, n3, 128, 32, 262144, big) == 0    # strict: generic
+    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, 0) == 0      # no workspace: generic
+    assert lib.spo_eval_path(2, 1, 0, n3, 64, 64, 262144, big) == 2     # fp64 too
+    assert lib.spo_eval_path(2, 0, 0, n3, 96, 1, 262144, big) == 1      # rows not 512-byte multiples
+    need = lib.spo_eval_workspace_bytes(2, 0, 0, 262144)
+    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, need) == 2
+    monkeypatch.setenv("SPO_LINE", "0")
+    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, big) == 1
+    assert lib.spo_eval_path(9, 0, 0, n3, 128, 32, 262144, big) == -1
 
 
 def test_error_codes_map_to_reference_exceptions(lib):
