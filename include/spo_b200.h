@@ -131,7 +131,8 @@ int spo_eval_lanes(int kind, int dtype, int mode, const void *table, const int32
  *   SPO_PATH_GENERIC  one-pass kernel (strict mode, no workspace, small batches)
  *   SPO_PATH_TMA      per-position TMA pipeline (spo_eval_tma.cu)
  *   SPO_PATH_LINE     line-window kernel: planes shared along grid lines, for
- *                     batches of >= 0.5 positions per grid cell (spo_eval_line.cu)
+ *                     VGL/VGH batches of >= 1 position per grid cell
+ *                     (spo_eval_line.cu)
  * -1 on bad arguments.  All paths give bitwise identical results.
  */
 #define SPO_PATH_GENERIC 0

@@ -322,17 +322,19 @@ extern "C" int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64
     return a > b ? a : b;
 }
 
-// positions per grid cell from which the line-window kernel is used (NUM/DEN):
-// sustained-rate crossover measured by scripts/micro/line_sustained.py
-constexpr long long LINE_DENSITY_NUM = 1, LINE_DENSITY_DEN = 2;
+// positions per grid cell from which the line-window kernel is used (NUM/DEN),
+// for VGL and VGH: sustained-rate crossover measured by
+// scripts/micro/line_sustained.py (V has too little math per plane to pay
+// for the plane-sharing protocol)
+constexpr long long LINE_DENSITY_NUM = 1, LINE_DENSITY_DEN = 1;
 
 // line-window kernel for batches dense enough to share stencil planes along
 // grid lines (SPO_LINE=0/1 forces it off/on; read on every call)
-static bool want_line(const int32_t *n3, long long n_pos) {
+static bool want_line(int kind, const int32_t *n3, long long n_pos) {
     const char *env_line = getenv("SPO_LINE");
     if (env_line) return env_line[0] == '1';
     const long long cells = (long long)n3[0] * n3[1] * n3[2];
-    return n_pos * LINE_DENSITY_DEN >= cells * LINE_DENSITY_NUM;
+    return kind != SPO_KIND_V && n_pos * LINE_DENSITY_DEN >= cells * LINE_DENSITY_NUM;
 }
 
 // lane_limit < 0: every table lane is stored and `out` must be memory of the
@@ -394,7 +396,7 @@ static int eval_impl(int kind, int dtype, int mode, const void *table, const int
                 g.delta[ax] = delta3[ax];
                 g.n[ax] = n3[ax];
             }
-            if (want_line(n3, n_pos)) {
+            if (want_line(kind, n3, n_pos)) {
                 const int r = eval_line(kind, dtype, table, geo, g, pos, n_pos, out, out_pos_stride,
                                         out_stream_stride, reinterpret_cast<const long long *>(out_index), status,
                                         workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream), lanes);
@@ -482,7 +484,7 @@ extern "C" int spo_eval_path(int kind, int dtype, int mode, const int32_t *n3, i
     if (mode != SPO_MODE_FAST || workspace_bytes <= 0) return SPO_PATH_GENERIC;
     const char *env_tma = getenv("SPO_TMA");
     if (env_tma && env_tma[0] == '0') return SPO_PATH_GENERIC;
-    if (want_line(n3, n_pos) && eval_line_eligible(dtype, geo, n_pos, workspace_bytes)) return SPO_PATH_LINE;
+    if (want_line(kind, n3, n_pos) && eval_line_eligible(dtype, geo, n_pos, workspace_bytes)) return SPO_PATH_LINE;
     if (workspace_bytes >= eval_tma_workspace_bytes(dtype, n_pos) && n_pos < (1LL << 31)) return SPO_PATH_TMA;
     return SPO_PATH_GENERIC;
 }

@@ -33,13 +33,15 @@ def main():
     n_grid, n = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (64, 4096)
     kind = sys.argv[3] if len(sys.argv) > 3 else "vgh"
     dens = [float(x) for x in sys.argv[4].split(",")] if len(sys.argv) > 4 else [0.1, 0.25, 0.5, 1.0]
-    dt = DeviceTable.random(unit_cell_grid(n_grid), n, seed=1)
+    f64 = len(sys.argv) > 5 and sys.argv[5] == "f64"
+    dt = (DeviceTable.normal_f64(unit_cell_grid(n_grid), n, seed=1) if f64
+          else DeviceTable.random(unit_cell_grid(n_grid), n, seed=1))
     cells = n_grid ** 3
     S = {"v": 1, "vgl": 5, "vgh": 10}[kind]
     for d in dens:
         P = int(d * cells)
         pos = torch.from_numpy(np.random.default_rng(P).random((P, 3))).cuda()
-        out = torch.empty((P, S, dt.lanes), device="cuda")
+        out = torch.empty((P, S, dt.lanes), device="cuda", dtype=torch.float64 if f64 else torch.float32)
         res = {}
         for v in ("0", "1", "0", "1"):
             os.environ["SPO_LINE"] = v
@@ -63,7 +65,8 @@ def main():
             e1.synchronize()
             ms = e0.elapsed_time(e1) / k
             res.setdefault("line" if v == "1" else "tma", []).append((round(ms, 3), clk))
-        print(json.dumps({"grid": n_grid, "N": n, "kind": kind, "density": d, "P": P, "ms_mhz_w": res}), flush=True)
+        print(json.dumps({"grid": n_grid, "N": n, "kind": kind, "dtype": "f64" if f64 else "f32", "density": d,
+                          "P": P, "ms_mhz_w": res}), flush=True)
 
 
 if __name__ == "__main__":
