@@ -4,7 +4,7 @@ template): orbital-evals/s, algorithmic GB/s and the fraction of the measured
 HBM bandwidth, per kernel kind.  Inputs are generated on the device with the
 reference's streams (table: FillSpec.random(0); positions: walker streams,
 seed 1).  Timing: CUDA events around each config's launches after a warm-up
-pass, best of `--reps` repetitions.
+pass: sustained back-to-back calls (see timed()), the regime of bench.py.
 
     python scripts/bench_configs.py [--configs 1,2,3,4,5] [--reps 3] [--md out.md]
 """
@@ -22,18 +22,32 @@ sys.path.insert(0, ROOT)
 
 
 def timed(fn, reps):
+    """Sustained rate, the regime of bench.py's timed region: ~0.3 s of warm-up
+    calls (clocks settle under the power controller), then `reps` x ~0.4 s of
+    back-to-back calls timed with CUDA events; the mean seconds per call of the
+    fastest window."""
+    import time
+
     import torch
 
     fn()
     torch.cuda.synchronize()
+    t0, k = time.perf_counter(), 0
+    while time.perf_counter() - t0 < 0.3 or k < 2:
+        fn()
+        torch.cuda.synchronize()
+        k += 1
+    per = (time.perf_counter() - t0) / k
+    n = max(2, int(0.4 / per))
     best = float("inf")
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        fn()
+        for _ in range(n):
+            fn()
         e1.record()
         e1.synchronize()
-        best = min(best, e0.elapsed_time(e1) * 1e-3)
+        best = min(best, e0.elapsed_time(e1) * 1e-3 / n)
     return best
 
 
@@ -52,7 +66,7 @@ def main():
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         peak = float(json.load(f)["hbm_gbs"])
     rows = []
-    chunk = 1 << 17
+    chunk = 1 << 18  # positions per launch, as bench.py
     for idx in [int(c) for c in args.configs.split(",")]:
         cfg = CONFIGS[idx]
         if cfg.dtype == "f64":
