@@ -1,31 +1,31 @@
-// spo_eval_line.cu -- the line-window kernel: the FAST path for large batches
-// (fp32 and fp64).  Same per-orbital arithmetic as spo_eval_tma.cu (bitwise),
-// different data movement: stencil planes are shared between positions.
+// spo_eval_line.cu -- the line-window kernel: the FAST path for dense VGL /
+// VGH batches (fp32 and fp64).  Same per-orbital arithmetic as
+// spo_eval_tma.cu (bitwise), different data movement: stencil planes are
+// shared between positions.
 //
 // Position p's 4x4x4 stencil is four planes i0..i0+3 of 4(j) x 4(k) rows.  Two
 // positions on the same grid line (j0, k0) with i0 values less than 4 apart
 // share planes.  So:
 //
-//  1. line_keys_kernel + cub radix sort + line_records_kernel: positions are
-//     sorted by (spatial block, j0, k0, i0) -- the 4x4x4 block order of
-//     spo_eval_tma.cu's bucketing for L2 locality, and inside a block whole
-//     lines in increasing i0 -- into records (36 weights, cell, original
-//     index).
+//  1. line_keys_kernel + cub radix sort + line_records_kernel +
+//     line_runs_kernel: positions are sorted by (spatial block, j0, k0, i0) --
+//     the 4x4x4 block order of spo_eval_tma.cu's bucketing for L2 locality,
+//     and inside a block whole lines in increasing i0 -- into records (36
+//     weights, cell, original index); every run of BPL sorted positions gets
+//     the list of planes it needs in load order and each record the number of
+//     its i0 plane within that list.
 //  2. line_kernel: persistent CTAs (one per SM).  A work item is (unit u = a
-//     2 KB-wide slice of every table row: 512 fp32 / 256 fp64 lanes, run of up
-//     to BPL sorted positions), handed out by a global ticket in unit-major
-//     order.  One producer warp walks the run and loads each plane the run
-//     needs ONCE, in line order (plane = 16 rows x 2 KB = 32 KB as four
-//     512-byte-wide TMA boxes), into a 6-slot shared-memory ring; eight
-//     consumer warps (64 fp32 / 32 fp64 lanes each) evaluate every position of
-//     the run from the ring and release planes no later position needs
-//     (mbarrier full/empty pairs per slot).  With one position per cell along
-//     a line, a position needs ~1.2 new planes instead of 4: L2->SM traffic
-//     and the TMA shared-memory writes drop ~3x.
+//     512-byte slice of every table row: 128 fp32 / 64 fp64 lanes, run), handed
+//     out by a global ticket in unit-major order.  A producer warp loads each
+//     plane of the run ONCE (one 16-row TMA box) into a 24-slot shared-memory
+//     ring; consumer warp g evaluates positions g, g + CONS, ... of the run
+//     from the ring.  With one position per cell along a line, a position
+//     needs ~1.2 new planes instead of 4: L2->SM traffic drops ~3.4x.
 //
-// The producer and the consumers derive the same plane sequence from the
-// records (plane_step below), so no plane ids are exchanged: plane number s
-// lives in slot s % R, phase s / R.
+// Synchronisation: one full mbarrier per slot (TMA complete_tx); the producer
+// publishes how many planes are armed (`issued`), each consumer the first
+// plane it will still need (`relw[g]`); see the kernel body for why neither
+// side can alias an mbarrier phase or deadlock.
 #include <cuda.h>
 
 #include <cub/device/device_radix_sort.cuh>
