@@ -30,3 +30,19 @@ def test_graph_replay_bitwise(pipeline, dtype):
     with pytest.raises(DomainError):
         g.run(bad, check=True)
     g.run(rng.random((1000, 3)), check=True)  # status is reset by every replay
+
+
+def test_graph_replay_line_path():
+    """A dense batch (line-window kernel: cub sort + records + runs + line
+    kernel) captured and replayed bitwise."""
+    import torch
+
+    from paper_1611_02665_b200.kernels import eval_path
+
+    dt = DeviceTable.random(unit_cell_grid(8), 256, seed=2)
+    assert eval_path(dt, "vgh", 3000) == "line"
+    g = GraphedEvaluator(dt, "vgh", 3000)
+    rng = np.random.default_rng(3)
+    for _ in range(3):
+        pos = rng.random((3000, 3))
+        assert torch.equal(g.run(pos).clone(), evaluate(dt, "vgh", pos))
