@@ -56,21 +56,44 @@ constexpr int MAX_AXIS = 256;                    // cell index fits 8 bits of th
 
 template <typename T>
 struct LT;
-// CONS consumer warps (+ one producer warp); consumer warp w evaluates the
-// positions q = w (mod CONS) of every run over the whole unit (one 16-byte
-// lane vector per thread: 4 fp32 / 2 fp64 orbitals)
+// Warp-specialised with register reallocation (setmaxnreg, per warpgroup):
+// warpgroup 0 is the producer group (warp 0 produces, warps 1-3 retire) and
+// shrinks to PREG registers; the CONS = 4 x (WGS - 1) consumer warps grow to
+// CREG.  Consumer warp w evaluates positions q = w (mod CONS) of every run
+// over the whole unit (one 16-byte lane vector per thread: 4 fp32 / 2 fp64
+// orbitals).  Budget: 128 x PREG + CONS x 32 x CREG <= the CTA's launch
+// allocation (regs_fit below).
 template <>
 struct LT<float> {
     static constexpr int RECB = 36 * 4 + 16;
-    static constexpr int CONS = 11;  // + the producer: 12 warps, 3 per SMSP (13 would cap at 128 registers)
-    static constexpr int R = 24;     // plane slots
+    static constexpr int WGS = 4;     // 12 consumer warps, 3 per SMSP
+    static constexpr int PREG = 32, CREG = 160;
+    static constexpr int R = 24;      // plane slots
 };
 template <>
 struct LT<double> {
     static constexpr int RECB = 36 * 8 + 16;
-    static constexpr int CONS = 7;   // fp64 weights need ~200 registers
-    static constexpr int R = 22;     // plane slots (larger records)
+    static constexpr int WGS = 3;     // 8 consumer warps: fp64 weights need ~200 registers
+    static constexpr int PREG = 40, CREG = 232;
+    static constexpr int R = 22;      // plane slots (larger records)
 };
+template <typename T>
+constexpr int cons_warps() {
+    return 4 * (LT<T>::WGS - 1);
+}
+template <typename T>
+constexpr int threads() {
+    return 128 * LT<T>::WGS;
+}
+// The pool setmaxnreg redistributes is the CTA's launch allocation: threads x
+// the per-thread count __launch_bounds__ gives (64K / threads, rounded down to
+// a multiple of 8).  Growing past it would make TRY_ALLOC spin forever.
+template <typename T>
+constexpr bool regs_fit() {
+    return 128 * LT<T>::PREG + 32 * cons_warps<T>() * LT<T>::CREG <= threads<T>() * (65536 / threads<T>() / 8 * 8);
+}
+static_assert(regs_fit<float>(), "fp32 register split exceeds the launch allocation");
+static_assert(regs_fit<double>(), "fp64 register split exceeds the launch allocation");
 
 struct LArgs {
     const unsigned char *recs;  // [n_pos][RECB], sorted
@@ -201,9 +224,9 @@ static_assert(smem_bytes<double>() <= 232448, "shared memory budget");
 
 // ---------------------------------------------------------------- kernel --
 template <int KIND, typename T>
-__global__ void __launch_bounds__((LT<T>::CONS + 1) * 32, 1) line_kernel(const __grid_constant__ CUtensorMap tmap, const LArgs a) {
+__global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_constant__ CUtensorMap tmap, const LArgs a) {
     constexpr int S = NS<KIND>::S;
-    constexpr int CONSUMERS = LT<T>::CONS;
+    constexpr int CONSUMERS = cons_warps<T>();
     constexpr int R = LT<T>::R;
     constexpr int W = 16 / (int)sizeof(T);         // lanes per thread (16-byte vector)
     constexpr int RECB = LT<T>::RECB;
@@ -237,8 +260,10 @@ __global__ void __launch_bounds__((LT<T>::CONS + 1) * 32, 1) line_kernel(const _
     }
     __syncthreads();
 
-    if (warp == CONSUMERS) {
+    if (warp < 4) {
         // ------------------------------------------------------ producer --
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(LT<T>::PREG));
+        if (warp != 0) return;
         // lane 0 takes tickets and loads run records + plane lists; lanes
         // 0..PBATCH-1 issue the run's planes PBATCH at a time (one slot each)
         const unsigned long long policy = l2_policy(a.evict_last);
@@ -341,7 +366,8 @@ __global__ void __launch_bounds__((LT<T>::CONS + 1) * 32, 1) line_kernel(const _
     // only on its own planes: `issued` says a plane's slot is armed (so the
     // parity wait is on the right phase), and relw[g] publishes the first
     // plane it will need next (all below are free for the producer).
-    const int g = warp;
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(LT<T>::CREG));
+    const int g = warp - 4;
     unsigned base = 0;
     auto publish = [&](unsigned v) {
         __syncwarp();
@@ -417,7 +443,7 @@ static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t 
     int grid = (int)min((long long)sms, a.n_items);
     if (grid < 1) grid = 1;
     cudaFuncSetAttribute(line_kernel<KIND, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    line_kernel<KIND, T><<<grid, (LT<T>::CONS + 1) * 32, sm, st>>>(map, a);
+    line_kernel<KIND, T><<<grid, threads<T>(), sm, st>>>(map, a);
     return check_launch("spo_eval (line) launch");
 }
 
