@@ -19,7 +19,8 @@
 //     out by a global ticket in unit-major order.  A producer warp loads each
 //     plane of the run ONCE (one 16-row TMA box) into a 24-slot shared-memory
 //     ring; consumer warp g evaluates positions g, g + CONS, ... of the run
-//     from the ring.  With one position per cell along a line, a position
+//     from the ring (warp-specialised: the producer warpgroup hands its
+//     registers to the consumers with setmaxnreg).  With one position per cell along a line, a position
 //     needs ~1.2 new planes instead of 4: L2->SM traffic drops ~3.4x.
 //
 // Synchronisation: one full mbarrier per slot (TMA complete_tx); the producer
