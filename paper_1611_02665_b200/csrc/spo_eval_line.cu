@@ -455,13 +455,25 @@ static size_t pad256(size_t b) { return (b + 255) / 256 * 256; }
 // Workspace of the line path: [header][keys in/out][order in/out][cub temp]
 // [records].  The radix-sort temp size is only known on a device; the bound
 // below covers it (checked at call time).
-static long long line_cub_bound(long long n) { return (4LL << 20) + (long long)line::pad256(4 * (size_t)n); }
+// Radix-sort temp storage: exact when a device answers cub's size query
+// (the double-buffer variant: ping-pong in our key/value buffers, the temp
+// holds histograms and look-back state only), else a generous bound.
+static long long line_cub_bytes(long long n) {
+    size_t bytes = 0;
+    cub::DoubleBuffer<unsigned> keys(nullptr, nullptr);
+    cub::DoubleBuffer<int> vals(nullptr, nullptr);
+    if (n > 0 && n < (1LL << 31) &&
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, vals, (int)n, 0, 32) == cudaSuccess)
+        return (long long)line::pad256(bytes);
+    cudaGetLastError();
+    return (8LL << 20) + (long long)line::pad256((size_t)n);
+}
 
 long long eval_line_workspace_bytes(int dtype, long long n_pos) {
     using namespace line;
     const long long recb = dtype == SPO_F64 ? LT<double>::RECB : LT<float>::RECB;
     const long long runs = (n_pos + BPL - 1) / BPL;
-    return WS_HEADER + 4 * (long long)pad256(4 * n_pos) + line_cub_bound(n_pos) + (long long)pad256(n_pos * recb) +
+    return WS_HEADER + 4 * (long long)pad256(4 * n_pos) + line_cub_bytes(n_pos) + (long long)pad256(n_pos * recb) +
            runs * PLB;
 }
 
@@ -513,17 +525,18 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     int *vals_in = reinterpret_cast<int *>(ws + WS_HEADER + 2 * vec);
     int *vals_out = reinterpret_cast<int *>(ws + WS_HEADER + 3 * vec);
     unsigned char *temp = ws + WS_HEADER + 4 * vec;
+    cub::DoubleBuffer<unsigned> keys(keys_in, keys_out);
+    cub::DoubleBuffer<int> vals(vals_in, vals_out);
     size_t temp_bytes = 0;
-    if (cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)n_pos, 0, 32,
-                                        st) != cudaSuccess) {
+    if (cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, vals, (int)n_pos, 0, 32, st) != cudaSuccess) {
         cudaGetLastError();
         return -1;
     }
-    if ((long long)temp_bytes > line_cub_bound(n_pos)) return -1;
-    unsigned char *recs = temp + line_cub_bound(n_pos);
+    const long long temp_room = line_cub_bytes(n_pos);
+    if ((long long)temp_bytes > temp_room) return -1;
+    unsigned char *recs = temp + temp_room;
     int *plist = reinterpret_cast<int *>(recs + pad256((size_t)n_pos * (dtype == SPO_F64 ? LT<double>::RECB
                                                                                           : LT<float>::RECB)));
-
     CUtensorMap map;
     cuuint64_t dims[5] = {(cuuint64_t)geo.nb, (cuuint64_t)geo.nzp, (cuuint64_t)geo.nyp, (cuuint64_t)geo.nxp,
                           (cuuint64_t)geo.n_tiles};
@@ -540,15 +553,15 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     if (cudaMemsetAsync(ws, 0, WS_HEADER, st) != cudaSuccess) return check_launch("workspace reset");
     const long long blocks = min((n_pos + 255) / 256, 148LL * 16);
     line_keys_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, keys_in, vals_in, status);
-    if (cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)n_pos, 0, 32,
-                                        st) != cudaSuccess)
+    if (cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, vals, (int)n_pos, 0, 32, st) != cudaSuccess)
         return check_launch("spo_eval (line sort)");
+    const int *order = vals.Current();  // the sorted original indices (either buffer)
     const unsigned run_blocks = (unsigned)((n_pos + (long long)BPL * 128 - 1) / ((long long)BPL * 128));
     if (dtype == SPO_F64) {
-        line_records_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(g, pos, vals_out, n_pos, recs);
+        line_records_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(g, pos, order, n_pos, recs);
         line_runs_kernel<double><<<run_blocks, 128, 0, st>>>(n_pos, recs, plist);
     } else {
-        line_records_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(g, pos, vals_out, n_pos, recs);
+        line_records_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(g, pos, order, n_pos, recs);
         line_runs_kernel<float><<<run_blocks, 128, 0, st>>>(n_pos, recs, plist);
     }
     int rc = check_launch("spo_eval (line prologue)");

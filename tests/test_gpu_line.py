@@ -124,3 +124,18 @@ def test_line_large_grid_falls_back(monkeypatch):
     pos = np.random.default_rng(1).random((9000, 3))
     a, b = _both(monkeypatch, dt, "v", pos)
     assert _eq(a, b)
+
+
+def test_line_large_batch(monkeypatch):
+    """2.1M positions (64 per cell, many full runs of one cell): the radix
+    sort's double buffers and the exact workspace query at scale."""
+    import torch
+
+    from paper_1611_02665_b200.kernels import eval_path
+
+    dt = DeviceTable.random(unit_cell_grid(32), 128, seed=6)
+    P = 2_100_000
+    assert eval_path(dt, "vgl", P) == "line"
+    pos = torch.from_numpy(np.random.default_rng(10).random((P, 3))).cuda()
+    a, b = _both(monkeypatch, dt, "vgl", pos)
+    assert _eq(a, b)
