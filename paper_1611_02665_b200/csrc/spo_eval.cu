@@ -305,7 +305,9 @@ long long eval_line_workspace_bytes(int dtype, long long n_pos);
 bool eval_line_eligible(int dtype, const TableGeom &geo, long long n_pos, long long ws_bytes);
 int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, const GridArgs &g, const double *pos,
               long long n_pos, void *out, long long ops, long long oss, const long long *out_index, int *status,
-              void *workspace, long long ws_bytes, cudaStream_t st, long long lane_limit);
+              void *workspace, long long ws_bytes, cudaStream_t st, long long lane_limit,
+              const void *coef = nullptr, long long coef_stride = 0, double *ratios = nullptr,
+              long long ratio_bytes = 0);
 long long eval_tma_ratio_bytes(int kind, int dtype, long long nb, long long n_tiles, long long n_pos);
 }
 
@@ -515,7 +517,8 @@ extern "C" int64_t spo_eval_ratios_workspace_bytes(int kind, int dtype, int32_t 
     if (dtype != SPO_F32 && dtype != SPO_F64) return -1;
     const long long extra = eval_tma_ratio_bytes(kind, dtype, nb, n_tiles, n_pos);
     if (extra < 0) return -1;
-    return eval_tma_workspace_bytes(dtype, n_pos) + extra;
+    const long long a = eval_tma_workspace_bytes(dtype, n_pos), b = eval_line_workspace_bytes(dtype, n_pos);
+    return (a > b ? a : b) + extra;
 }
 
 extern "C" int spo_eval_ratios(int kind, int dtype, const void *table, const int32_t *n3, int32_t nb,
@@ -552,6 +555,17 @@ extern "C" int spo_eval_ratios(int kind, int dtype, const void *table, const int
         g.cnt[ax] = (double)n3[ax];
         g.delta[ax] = delta3[ax];
         g.n[ax] = n3[ax];
+    }
+    // The line kernel's ratio epilogue only when forced (SPO_LINE=1): without
+    // the output stream the per-position kernel is not power-bound, and it is
+    // faster (scripts/bench_ratios.py: 6.30e10 vs 6.18e10 orbital-evals/s).
+    const char *env_line = getenv("SPO_LINE");
+    if (env_line && env_line[0] == '1') {
+        const long long extra = eval_tma_ratio_bytes(kind, dtype, nb, n_tiles, n_pos);
+        rc = eval_line(kind, dtype, table, geo, g, pos, n_pos, nullptr, 0, 0, nullptr, status, workspace,
+                       workspace_bytes, reinterpret_cast<cudaStream_t>(stream), 0, coef, coef_stride, ratios,
+                       extra);
+        if (rc >= 0) return rc;
     }
     rc = eval_tma(kind, dtype, table, geo, g, pos, n_pos, nullptr, 0, 0, nullptr, status, workspace,
                   workspace_bytes, reinterpret_cast<cudaStream_t>(stream), 0, 0, coef, coef_stride, ratios);

@@ -109,6 +109,11 @@ struct LArgs {
     const long long *out_index;
     long long lane_limit;
     int evict_last;
+    // fused ratio epilogue (RATIO kernels, spo_eval_ratios): per (unit,
+    // position) partial dot products of every stream with the coefficient row
+    const void *coef;           // [n_pos][coef_stride] in output-lane layout
+    long long coef_stride;
+    double *partials;           // [units][n_pos][S]
 };
 
 struct LItem {
@@ -224,7 +229,7 @@ static_assert(smem_bytes<float>() <= 232448, "shared memory budget");
 static_assert(smem_bytes<double>() <= 232448, "shared memory budget");
 
 // ---------------------------------------------------------------- kernel --
-template <int KIND, typename T>
+template <int KIND, typename T, bool RATIO>
 __global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_constant__ CUtensorMap tmap, const LArgs a) {
     constexpr int S = NS<KIND>::S;
     constexpr int CONSUMERS = cons_warps<T>();
@@ -401,10 +406,17 @@ __global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_cons
                 for (int h = 0; h < AN; ++h) zero(acc[s][h]);
             if (cell.x < 0) {
                 publish(first_plane(q + CONSUMERS));
-                if (nv == W)
+                if constexpr (RATIO) {
+                    if (lane == 0) {
+                        double *dst = a.partials + ((long long)it.u * a.n_pos + cell.w) * S;
+#pragma unroll
+                        for (int s = 0; s < S; ++s) dst[s] = (double)NAN;
+                    }
+                } else if (nv == W) {
                     store_lane<S>(o, a.out_stream_stride, acc, false);
-                else if (nv > 0)
+                } else if (nv > 0) {
                     store_lane_partial<S>(o, a.out_stream_stride, acc, false, nv);
+                }
                 continue;
             }
             const unsigned s0 = base + (unsigned)(cell.z & 0xffff);
@@ -427,10 +439,22 @@ __global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_cons
                 slab_contract<KIND, BOXL>(p, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
             }
             publish(first_plane(q + CONSUMERS));  // this position's planes are read
-            if (nv == W)
+            if constexpr (RATIO) {
+                // the warp's 32 lanes are this position's unit: dot with the
+                // coefficient row, reduced over the warp (as spo_eval_tma.cu)
+                const T *cf = reinterpret_cast<const T *>(a.coef) + (long long)cell.w * a.coef_stride + L0;
+                double part[S];
+                ratio_partials<S, 32>(acc, cf, true, part);
+                if (lane == 0) {
+                    double *dst = a.partials + ((long long)it.u * a.n_pos + cell.w) * S;
+#pragma unroll
+                    for (int s = 0; s < S; ++s) dst[s] = part[s];
+                }
+            } else if (nv == W) {
                 store_lane<S>(o, a.out_stream_stride, acc, true);
-            else if (nv > 0)
+            } else if (nv > 0) {
                 store_lane_partial<S>(o, a.out_stream_stride, acc, true, nv);
+            }
         }
         base += count;
         __syncwarp();
@@ -438,14 +462,18 @@ __global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_cons
     }
 }
 
-template <int KIND, typename T>
+template <int KIND, typename T, bool RATIO>
 static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
     constexpr size_t sm = smem_bytes<T>();
     int grid = (int)min((long long)sms, a.n_items);
     if (grid < 1) grid = 1;
-    cudaFuncSetAttribute(line_kernel<KIND, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    line_kernel<KIND, T><<<grid, threads<T>(), sm, st>>>(map, a);
+    cudaFuncSetAttribute(line_kernel<KIND, T, RATIO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    line_kernel<KIND, T, RATIO><<<grid, threads<T>(), sm, st>>>(map, a);
     return check_launch("spo_eval (line) launch");
+}
+template <int KIND, typename T>
+static int launch_r(bool ratio, const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
+    return ratio ? launch<KIND, T, true>(map, a, sms, st) : launch<KIND, T, false>(map, a, sms, st);
 }
 
 static size_t pad256(size_t b) { return (b + 255) / 256 * 256; }
@@ -508,11 +536,16 @@ bool eval_line_eligible(int dtype, const TableGeom &geo, long long n_pos, long l
 }
 
 // Returns -1 when the request is not taken (the caller falls back).
+int ratio_reduce(int kind, const double *partials, long long units, long long n_pos, double *ratios,
+                 cudaStream_t st);
+
 int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, const GridArgs &g, const double *pos,
               long long n_pos, void *out, long long ops, long long oss, const long long *out_index, int *status,
-              void *workspace, long long ws_bytes, cudaStream_t st, long long lane_limit) {
+              void *workspace, long long ws_bytes, cudaStream_t st, long long lane_limit, const void *coef,
+              long long coef_stride, double *ratios, long long ratio_bytes) {
     using namespace line;
-    if (!eval_line_eligible(dtype, geo, n_pos, ws_bytes) || !aligned16(workspace)) return -1;
+    const bool ratio = ratios != nullptr;
+    if (!eval_line_eligible(dtype, geo, n_pos, ws_bytes - ratio_bytes) || !aligned16(workspace)) return -1;
     EncodeTiledFn encode = line_encode();
     if (!encode) return -1;
     const int E = dtype == SPO_F64 ? 8 : 4;
@@ -584,18 +617,23 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     a.lane_limit = lane_limit;
     static const char *env_hint = getenv("SPO_L2HINT");
     a.evict_last = !(env_hint && env_hint[0] == '0');
+    a.coef = coef;
+    a.coef_stride = coef_stride;
+    a.partials = ratio ? reinterpret_cast<double *>(ws + eval_line_workspace_bytes(dtype, n_pos)) : nullptr;
 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (dtype == SPO_F64) {
-        if (kind == SPO_KIND_V) return launch<SPO_KIND_V, double>(map, a, sms, st);
-        if (kind == SPO_KIND_VGL) return launch<SPO_KIND_VGL, double>(map, a, sms, st);
-        return launch<SPO_KIND_VGH, double>(map, a, sms, st);
-    }
-    if (kind == SPO_KIND_V) return launch<SPO_KIND_V, float>(map, a, sms, st);
-    if (kind == SPO_KIND_VGL) return launch<SPO_KIND_VGL, float>(map, a, sms, st);
-    return launch<SPO_KIND_VGH, float>(map, a, sms, st);
+    if (dtype == SPO_F64)
+        rc = kind == SPO_KIND_V     ? launch_r<SPO_KIND_V, double>(ratio, map, a, sms, st)
+             : kind == SPO_KIND_VGL ? launch_r<SPO_KIND_VGL, double>(ratio, map, a, sms, st)
+                                    : launch_r<SPO_KIND_VGH, double>(ratio, map, a, sms, st);
+    else
+        rc = kind == SPO_KIND_V     ? launch_r<SPO_KIND_V, float>(ratio, map, a, sms, st)
+             : kind == SPO_KIND_VGL ? launch_r<SPO_KIND_VGL, float>(ratio, map, a, sms, st)
+                                    : launch_r<SPO_KIND_VGH, float>(ratio, map, a, sms, st);
+    if (rc || !ratio) return rc;
+    return ratio_reduce(kind, a.partials, units, n_pos, ratios, st);
 }
 
 }  // namespace spo

@@ -193,42 +193,6 @@ struct GroupDesc {
     int c0, m;
 };
 
-// Fused epilogue: this lane's orbitals dotted with its coefficient entries in
-// fp64, reduced over the LPP lanes of the position (xor shuffles stay inside
-// the lane segment), written once per (unit, position) by the segment leader.
-// fp32 tables: the lane's 4-term dot and the lane-segment reduction run in
-// fp32 (one chunk = at most 128 orbitals); chunks are summed in fp64.
-template <int S, int LPP>
-__device__ __forceinline__ void ratio_partials(const float2 (&acc)[S][2], const float *coef, bool live,
-                                               double (&part)[S]) {
-    float4 cf = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (live) cf = __ldg(reinterpret_cast<const float4 *>(coef));
-    float f[S];
-#pragma unroll
-    for (int s = 0; s < S; ++s)
-        f[s] = live ? __fmaf_rn(acc[s][1].y, cf.w,
-                                __fmaf_rn(acc[s][1].x, cf.z, __fmaf_rn(acc[s][0].y, cf.y, acc[s][0].x * cf.x)))
-                    : 0.0f;
-#pragma unroll
-    for (int off = LPP / 2; off > 0; off >>= 1)
-#pragma unroll
-        for (int s = 0; s < S; ++s) f[s] += __shfl_xor_sync(0xffffffffu, f[s], off);
-#pragma unroll
-    for (int s = 0; s < S; ++s) part[s] = f[s];
-}
-template <int S, int LPP>
-__device__ __forceinline__ void ratio_partials(const double2 (&acc)[S][1], const double *coef, bool live,
-                                               double (&part)[S]) {
-    double2 cf = make_double2(0.0, 0.0);
-    if (live) cf = __ldg(reinterpret_cast<const double2 *>(coef));
-#pragma unroll
-    for (int s = 0; s < S; ++s) part[s] = live ? __fma_rn(acc[s][0].y, cf.y, acc[s][0].x * cf.x) : 0.0;
-#pragma unroll
-    for (int off = LPP / 2; off > 0; off >>= 1)
-#pragma unroll
-        for (int s = 0; s < S; ++s) part[s] += __shfl_xor_sync(0xffffffffu, part[s], off);
-}
-
 template <int KIND, typename T, int CW, class C, bool RATIO>
 __global__ void __launch_bounds__(C::WARPS * 32, 1)
     eval_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Args a) {
@@ -524,6 +488,9 @@ long long eval_tma_ratio_bytes(int kind, int dtype, long long nb, long long n_ti
     return n_tiles * (row / 512) * n_pos * S * 8;
 }
 
+int ratio_reduce(int kind, const double *partials, long long units, long long n_pos, double *ratios,
+                 cudaStream_t st);
+
 // Called by spo_eval for FAST requests with a workspace.  Returns -1 when the
 // TMA path cannot be used (the caller then uses the generic kernel).
 // cw_request: chunk width in elements (0 = automatic).  With `ratios` set the
@@ -634,10 +601,16 @@ int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const
     const int rc = dtype == SPO_F64 ? launch_kind<double>(kind, cwb, ratio, map, a, sms, st)
                                     : launch_kind<float>(kind, cwb, ratio, map, a, sms, st);
     if (rc || !ratio) return rc;
+    return ratio_reduce(kind, a.partials, (long long)geo.n_tiles * a.chunks, n_pos, ratios, st);
+}
+
+// ratios[p][s] = sum over the units of partials[u][p][s] (fixed order)
+int ratio_reduce(int kind, const double *partials, long long units, long long n_pos, double *ratios,
+                 cudaStream_t st) {
     const int S = kind == SPO_KIND_V ? 1 : (kind == SPO_KIND_VGL ? 5 : 10);
     const long long n = n_pos * S;
     const long long blocks = min((n + 255) / 256, 148LL * 16);
-    ratio_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(a.partials, (long long)geo.n_tiles * a.chunks, n, ratios);
+    tma::ratio_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(partials, units, n, ratios);
     return check_launch("spo_eval_ratios (reduce) launch");
 }
 

@@ -273,5 +273,41 @@ __device__ __forceinline__ void store_lane_partial(double *o, long long sstride,
         if (nv > 0) o[s * sstride] = finite ? acc[s][0].x : NAN;
 }
 
+// Fused epilogue: this lane's orbitals dotted with its coefficient entries in
+// fp64, reduced over the LPP lanes of the position (xor shuffles stay inside
+// the lane segment), written once per (unit, position) by the segment leader.
+// fp32 tables: the lane's 4-term dot and the lane-segment reduction run in
+// fp32 (one chunk = at most 128 orbitals); chunks are summed in fp64.
+template <int S, int LPP>
+__device__ __forceinline__ void ratio_partials(const float2 (&acc)[S][2], const float *coef, bool live,
+                                               double (&part)[S]) {
+    float4 cf = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) cf = __ldg(reinterpret_cast<const float4 *>(coef));
+    float f[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+        f[s] = live ? __fmaf_rn(acc[s][1].y, cf.w,
+                                __fmaf_rn(acc[s][1].x, cf.z, __fmaf_rn(acc[s][0].y, cf.y, acc[s][0].x * cf.x)))
+                    : 0.0f;
+#pragma unroll
+    for (int off = LPP / 2; off > 0; off >>= 1)
+#pragma unroll
+        for (int s = 0; s < S; ++s) f[s] += __shfl_xor_sync(0xffffffffu, f[s], off);
+#pragma unroll
+    for (int s = 0; s < S; ++s) part[s] = f[s];
+}
+template <int S, int LPP>
+__device__ __forceinline__ void ratio_partials(const double2 (&acc)[S][1], const double *coef, bool live,
+                                               double (&part)[S]) {
+    double2 cf = make_double2(0.0, 0.0);
+    if (live) cf = __ldg(reinterpret_cast<const double2 *>(coef));
+#pragma unroll
+    for (int s = 0; s < S; ++s) part[s] = live ? __fma_rn(acc[s][0].y, cf.y, acc[s][0].x * cf.x) : 0.0;
+#pragma unroll
+    for (int off = LPP / 2; off > 0; off >>= 1)
+#pragma unroll
+        for (int s = 0; s < S; ++s) part[s] += __shfl_xor_sync(0xffffffffu, part[s], off);
+}
+
 }  // namespace tma
 }  // namespace spo

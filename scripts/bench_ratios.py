@@ -2,16 +2,20 @@
 """Throughput of the fused consumer epilogue (evaluate_ratios) vs evaluate()
 on config 4 (64^3, N=4096 fp32, VGH): orbital-evals/s with the [P][10][N]
 output stream (evaluate) and with the per-position ratios only (coef row of N
-floats in, 10 doubles out per position).  CUDA events, best of 3."""
+floats in, 10 doubles out per position).  Sustained back-to-back calls, as
+scripts/bench_configs.py (timed())."""
 import json
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 
 def main():
     import torch
+
+    from bench_configs import timed
 
     from paper_1611_02665_b200 import DeviceTable, evaluate, evaluate_ratios
     from paper_1611_02665_b200.workloads import CONFIGS, device_walker_positions
@@ -25,16 +29,7 @@ def main():
     res = {}
     for name, fn in (("evaluate (outputs to HBM)", lambda: evaluate(dt, "vgh", pos, out, check=False)),
                      ("evaluate_ratios (fused epilogue)", lambda: evaluate_ratios(dt, "vgh", pos, coef, check=False))):
-        fn()
-        torch.cuda.synchronize()
-        best = float("inf")
-        for _ in range(3):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            fn()
-            e1.record()
-            e1.synchronize()
-            best = min(best, e0.elapsed_time(e1) * 1e-3)
+        best = timed(fn, 3)
         res[name] = {"seconds": best, "orbital_evals_per_s": chunk * cfg.n_splines / best}
     print(json.dumps({"config": "cfg4 VGH, 262144 positions, N=4096", **res}, indent=1))
 

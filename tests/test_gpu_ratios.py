@@ -65,3 +65,34 @@ def test_ratios_untiled_and_errors(torch):
     bad[3, 0] = np.nan
     with pytest.raises(DomainError):
         evaluate_ratios(dt, "v", bad, coef)
+
+
+@pytest.mark.parametrize("kind,dtype", [("vgh", "f32"), ("vgl", "f32"), ("vgh", "f64")])
+def test_ratios_line_path(torch, monkeypatch, kind, dtype):
+    """Dense batches run the line-window kernel's ratio epilogue: bitwise equal
+    to the per-position kernel's (same lane dots, same warp reduction, same
+    fixed-order unit sum) and to the contraction of evaluate()'s outputs."""
+    grid = unit_cell_grid(16)
+    rng = np.random.default_rng(8)
+    if dtype == "f32":
+        dt = DeviceTable.random(grid, 256, seed=3)
+        tdt, rtol = torch.float32, 1e-6
+    else:
+        dt = DeviceTable.normal_f64(grid, 128, seed=3)
+        tdt, rtol = torch.float64, 1e-12
+    P = 12000  # ~3 positions per cell
+    pos = rng.random((P, 3))
+    pos[17] = np.nan
+    coef = torch.from_numpy(rng.standard_normal((P, dt.n_splines))).to("cuda", tdt)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    monkeypatch.setenv("SPO_LINE", "1")
+    a = evaluate_ratios(dt, kind, torch.from_numpy(pos).cuda(), coef, status=st, check=False)
+    monkeypatch.setenv("SPO_LINE", "0")
+    b = evaluate_ratios(dt, kind, torch.from_numpy(pos).cuda(), coef, check=False)
+    assert torch.equal(a.nan_to_num(7.0), b.nan_to_num(7.0)) and int(st.item()) == 1
+    assert bool(torch.isnan(a[17]).all())
+    ok = torch.ones(P, dtype=torch.bool)
+    ok[17] = False
+    monkeypatch.delenv("SPO_LINE")
+    want = reference_ratios(torch, dt, kind, pos[ok.numpy()], coef[ok.cuda()])
+    assert float((a[ok.cuda()] - want).abs().max() / want.abs().max()) < rtol
