@@ -97,9 +97,12 @@ const char *spo_last_error(void);
  *   workspace, workspace_bytes
  *           device scratch owned by the caller, at least
  *           spo_eval_workspace_bytes(kind, dtype, mode, n_pos) bytes, 16-byte
- *           aligned, not shared with a concurrent call.  With it, fp32 FAST
- *           calls run the TMA-pipelined kernel (per-position records + a work
- *           ticket); with NULL they run the generic kernel.  Same results.
+ *           aligned, not shared with a concurrent call.  With it, FAST calls
+ *           (fp32 and fp64) run the TMA-pipelined kernels: the line-window
+ *           kernel for VGL/VGH batches of >= 1 position per grid cell (planes
+ *           shared along grid lines), else the per-position kernel; with NULL
+ *           they run the generic kernel.  Bitwise identical results either way
+ *           (spo_eval_path tells which one runs).
  */
 int spo_eval(int kind, int dtype, int mode, const void *table, const int32_t *n3, int32_t nb,
              int32_t n_tiles, const double *dinv3, const double *delta3, const double *pos,
