@@ -27,6 +27,12 @@
  *                   walker Philox position streams, bit-identical, on device.
  *   spo_fill_normal_f64  builder-defined N(0,1) fill for the fp64 config
  *                   (no reference equivalent).
+ *   spo_eval_lanes  replaces the shared-output tile loop of the nested driver
+ *                   (driver.py:349-434) across GPUs: spo_eval storing only
+ *                   lanes [0, lane_limit) into (possibly peer) memory.
+ *   spo_eval_ratios beyond the reference: the consumer's contraction of every
+ *                   stream with a coefficient row, fused into the kernel.
+ *   spo_eval_path   which kernel spo_eval runs (no launch).
  *   spo_last_error  error text for the last failing call on this thread; the
  *                   Python host maps codes to the reference's exception types
  *                   (errors.py:4-17).
