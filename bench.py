@@ -2,7 +2,7 @@
 """Benchmark: B-spline VGH orbital-evals/s on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config 4] [--chunk 65536] [--mode fast] [--tile 0]
+                    [--config 4] [--chunk 0] [--mode fast] [--tile 0]
 
 Workload (default, BASELINE config 4 -- the VGH config with N >= 2048 the
 north-star roofline target names): 64^3 periodic grid (67^3 wrap-padded),
@@ -11,7 +11,10 @@ bit-identical to the reference's numpy fill), 4096 walkers x 256 moves =
 1,048,576 VGH positions per GPU per step (Philox walker streams, seed 1).
 A step evaluates all of them, in launches of `--chunk` positions into a
 reusable output buffer (every output is written to HBM; the reference also
-overwrites its output buffer per position, kernels.py:353-354).
+overwrites its output buffer per position, kernels.py:353-354).  --chunk 0
+(default): 524,288 positions per launch (2 per grid cell: more stencil planes
+shared by the line kernel) when the GPU has room for the 86 GB output buffer,
+else 262,144.
 
 Multi-GPU (torchrun, one rank per GPU): walker-sharded, table replicated,
 each rank evaluates its own 4096-walker population (weak scaling), no
@@ -51,7 +54,7 @@ def parse():
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--kind", default=None, help="override the config kernel (v/vgl/vgh)")
-    ap.add_argument("--chunk", type=int, default=1 << 18)
+    ap.add_argument("--chunk", type=int, default=0, help="positions per launch (0 = auto)")
     ap.add_argument("--mode", default="fast", choices=("fast", "strict"))
     ap.add_argument("--tile", type=int, default=-1, help="AoSoA tile size (-1 = auto, 0 = untiled)")
     ap.add_argument("--walkers", type=int, default=0, help="override walkers per GPU")
@@ -266,7 +269,12 @@ def run_b200(args):
     tile = "auto" if args.tile < 0 else (args.tile or None)
     table = DeviceTable.random(cfg.grid, N, seed=0, tile_size=tile, device=dev)
     pos = torch.from_numpy(pos_np).to(dev)
-    chunk = min(args.chunk, P)
+    chunk = args.chunk
+    if chunk <= 0:  # largest of 2^19 / 2^18 whose output buffer leaves 40 GB free
+        free, _ = torch.cuda.mem_get_info(dev)
+        per_pos = S * table.lanes * 4
+        chunk = 1 << 19 if free - (1 << 19) * per_pos > (40 << 30) else 1 << 18
+    chunk = min(chunk, P)
     out = torch.empty((chunk, S, table.lanes), dtype=torch.float32, device=dev)
     bounds = [(lo, min(P, lo + chunk)) for lo in range(0, P, chunk)]
     stream = torch.cuda.current_stream(dev)
@@ -360,6 +368,8 @@ def run_b200(args):
     }
 
     if rank == 0 and not args.no_e2e:
+        del out  # the drop-in path sizes its own scratch from the free memory
+        torch.cuda.empty_cache()
         result["e2e"] = e2e_dropin(table, kind, pos_np, N, S, eval_batch, WalkerOutputsSoA, args, dev)
         result["e2e_full_outputs"] = e2e_full_outputs(table, kind, pos_np, N, S, dev)
     if world > 1:
@@ -448,7 +458,7 @@ def ncu_traffic(args, cfg, kind, chunk, path):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             rec = json.load(f)
-        key = f"cfg{cfg.index}-{kind}-{args.mode}-tile{args.tile}-{path}"
+        key = f"cfg{cfg.index}-{kind}-{args.mode}-tile{args.tile}-{path}-{chunk}"
         r = rec.get(key)
         if r and r.get("positions_per_launch") == chunk:
             return r["dram_bytes_per_launch"]

@@ -411,9 +411,12 @@ def _as_positions(pos, check_finite: bool = True) -> np.ndarray:
     return arr
 
 
-# Drop-in path: positions per device pass, and the scratch bytes it may use.
-DROPIN_CHUNK = 1 << 18
-DROPIN_SCRATCH_BYTES = 48 << 30
+# Drop-in path: positions per device pass (2^19 = 2 per cell of a 64^3 grid:
+# the line kernel shares more planes), the scratch bytes it may use, and the
+# device memory it leaves free.
+DROPIN_CHUNK = 1 << 19
+DROPIN_SCRATCH_BYTES = 96 << 30
+DROPIN_FREE_RESERVE = 16 << 30
 # Batches larger than this are checked for non-finite positions on the device
 # (the kernels' status flag) instead of by a host pass; either way DomainError
 # is raised before the caller's buffers are touched.
@@ -428,7 +431,10 @@ def _eval_last(table, kind, pos: np.ndarray, mode: str):
     S = kind.output_streams_soa
     P = pos.shape[0]
     item = 8 if dt.dtype == np.float64 else 4
-    chunk = max(1, min(P, DROPIN_CHUNK, DROPIN_SCRATCH_BYTES // (S * dt.lanes * item)))
+    per_pos = S * dt.lanes * item
+    free = torch.cuda.mem_get_info(dt.device)[0]
+    budget = min(DROPIN_SCRATCH_BYTES, max(free - DROPIN_FREE_RESERVE, per_pos))
+    chunk = max(1, min(P, DROPIN_CHUNK, budget // per_pos))
     tdt = torch.float64 if dt.dtype == np.float64 else torch.float32
     scratch = torch.empty((chunk, S, dt.lanes), dtype=tdt, device=dt.device)
     status = torch.zeros(1, dtype=torch.int32, device=dt.device)

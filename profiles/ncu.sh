@@ -9,7 +9,7 @@ TAG=${1:-r01}
 shift || true
 mkdir -p gpurun_out
 CMD="python bench.py $*"
-SMALL="python bench.py --walkers 1024 --steps 1 --warmup 1 --no-cpu --no-e2e $*"
+SMALL="python bench.py --walkers 2048 --steps 1 --warmup 1 --no-cpu --no-e2e $*"
 $CMD > gpurun_out/bench_${TAG}.log 2>&1 || { echo "plain bench failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launches_${TAG}.log 2>&1
