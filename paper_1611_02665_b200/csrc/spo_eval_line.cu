@@ -505,24 +505,6 @@ long long eval_line_workspace_bytes(int dtype, long long n_pos) {
            runs * PLB;
 }
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn line_encode() {
-    static EncodeTiledFn fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeTiledFn>(p);
-    }
-    return fn;
-}
-
 // Whether the line path can take this request (layout, grid, workspace).
 bool eval_line_eligible(int dtype, const TableGeom &geo, long long n_pos, long long ws_bytes) {
     using namespace line;
@@ -546,8 +528,7 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     using namespace line;
     const bool ratio = ratios != nullptr;
     if (!eval_line_eligible(dtype, geo, n_pos, ws_bytes - ratio_bytes) || !aligned16(workspace)) return -1;
-    EncodeTiledFn encode = line_encode();
-    if (!encode) return -1;
+    if (!tensor_map_encoder()) return -1;
     const int E = dtype == SPO_F64 ? 8 : 4;
     const int boxl = BOXB / E;
 
@@ -571,17 +552,8 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     int *plist = reinterpret_cast<int *>(recs + pad256((size_t)n_pos * (dtype == SPO_F64 ? LT<double>::RECB
                                                                                           : LT<float>::RECB)));
     CUtensorMap map;
-    cuuint64_t dims[5] = {(cuuint64_t)geo.nb, (cuuint64_t)geo.nzp, (cuuint64_t)geo.nyp, (cuuint64_t)geo.nxp,
-                          (cuuint64_t)geo.n_tiles};
-    cuuint64_t strides[4] = {(cuuint64_t)geo.nb * E, (cuuint64_t)geo.nzp * geo.nb * E,
-                             (cuuint64_t)geo.nyp * geo.nzp * geo.nb * E, (cuuint64_t)geo.tile_stride * E};
-    cuuint32_t box[5] = {(cuuint32_t)boxl, 4, 4, 1, 1};
-    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    CUresult r = encode(&map, dtype == SPO_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5,
-                        const_cast<void *>(table), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    const int r = table_tensor_map(&map, table, geo, dtype, boxl);
+    if (r) return fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", r);
 
     if (cudaMemsetAsync(ws, 0, WS_HEADER, st) != cudaSuccess) return check_launch("workspace reset");
     const long long blocks = min((n_pos + 255) / 256, 148LL * 16);

@@ -394,24 +394,6 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
 }
 
 // ---------------------------------------------------------------- host --
-typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiled get_encode() {
-    static EncodeTiled fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeTiled>(p);
-    }
-    return fn;
-}
-
 template <typename T>
 constexpr size_t smem_bytes() {
     using C = typename TT<T>::Cfg;
@@ -507,8 +489,7 @@ int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const
     if (!workspace || ws_bytes < eval_tma_workspace_bytes(dtype, n_pos) + partial_bytes || !aligned16(workspace))
         return ratio ? fail(SPO_ERR_CONTRACT, "workspace too small for the ratio epilogue") : -1;
     if (n_pos >= (1LL << 31)) return -1;  // records carry 32-bit original indices
-    EncodeTiled encode = get_encode();
-    if (!encode) return ratio ? fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable") : -1;
+    if (!tensor_map_encoder()) return ratio ? fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable") : -1;
     if (ratio) cw_request = 512 / (dtype == SPO_F64 ? 8 : 4);
     const int E = dtype == SPO_F64 ? 8 : 4;
     // chunk width (bytes per row segment): one spatial block's rows x CW within
@@ -527,17 +508,8 @@ int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const
     const int cw = cwb / E;
 
     CUtensorMap map;
-    cuuint64_t dims[5] = {(cuuint64_t)geo.nb, (cuuint64_t)geo.nzp, (cuuint64_t)geo.nyp, (cuuint64_t)geo.nxp,
-                          (cuuint64_t)geo.n_tiles};
-    cuuint64_t strides[4] = {(cuuint64_t)geo.nb * E, (cuuint64_t)geo.nzp * geo.nb * E,
-                             (cuuint64_t)geo.nyp * geo.nzp * geo.nb * E, (cuuint64_t)geo.tile_stride * E};
-    cuuint32_t box[5] = {(cuuint32_t)cw, 4, 4, 1, 1};
-    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    CUresult r = encode(&map, dtype == SPO_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                        5, const_cast<void *>(table), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    const int r = table_tensor_map(&map, table, geo, dtype, cw);
+    if (r) return fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", r);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

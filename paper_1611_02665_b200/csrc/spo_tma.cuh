@@ -6,6 +6,46 @@
 #include "spo_common.cuh"
 
 namespace spo {
+
+// ---- host: the 5-D TMA descriptor of a device table -- dims (lanes, k', j',
+// i', tile), box (box_lanes, 4, 4, 1, 1): one box = one (position, i) slab.
+// Returns 0, -1 when the driver has no cuTensorMapEncodeTiled, or the
+// CUresult of a failed encode.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn tensor_map_encoder() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+inline int table_tensor_map(CUtensorMap *map, const void *table, const TableGeom &geo, int dtype, int box_lanes) {
+    EncodeTiledFn encode = tensor_map_encoder();
+    if (!encode) return -1;
+    const cuuint64_t E = dtype == SPO_F64 ? 8 : 4;
+    cuuint64_t dims[5] = {(cuuint64_t)geo.nb, (cuuint64_t)geo.nzp, (cuuint64_t)geo.nyp, (cuuint64_t)geo.nxp,
+                          (cuuint64_t)geo.n_tiles};
+    cuuint64_t strides[4] = {(cuuint64_t)geo.nb * E, (cuuint64_t)geo.nzp * geo.nb * E,
+                             (cuuint64_t)geo.nyp * geo.nzp * geo.nb * E, (cuuint64_t)geo.tile_stride * E};
+    cuuint32_t box[5] = {(cuuint32_t)box_lanes, 4, 4, 1, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    const CUresult r =
+        encode(map, dtype == SPO_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5,
+               const_cast<void *>(table), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : (int)r;
+}
+
 namespace tma {
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
