@@ -210,9 +210,12 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
     out_index  optional int64 CUDA tensor: position p is written to out[out_index[p]]
     status     optional int32 CUDA tensor(1): set to 1 on a non-finite position
     check      raise DomainError for non-finite positions (one sync on status)
-    pipeline   fp32 fast mode: True = TMA-pipelined kernel (needs a workspace,
-               allocated here), False = the generic kernel (same bits),
-               "auto" = pipelined when P * lanes >= PIPELINE_MIN_WORK
+    pipeline   fast mode: True = the TMA-pipelined kernels (a workspace is
+               allocated here; the line-window kernel for VGL/VGH batches of
+               >= 1 position per grid cell, else the per-position kernel),
+               False = the generic kernel, "auto" = pipelined when
+               P * lanes >= PIPELINE_MIN_WORK.  Same bits either way
+               (eval_path() tells which kernel runs)
     lane_limit store only output lanes [0, lane_limit) (spo_eval_lanes); `out`
                is then required and may live on another GPU (a peer
                device's memory or an IPC mapping of it): the fused
