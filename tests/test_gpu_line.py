@@ -139,3 +139,15 @@ def test_line_large_batch(monkeypatch):
     pos = torch.from_numpy(np.random.default_rng(10).random((P, 3))).cuda()
     a, b = _both(monkeypatch, dt, "vgl", pos)
     assert _eq(a, b)
+
+
+@pytest.mark.parametrize("dtype,tile", [("f32", 256), ("f64", None)])
+def test_line_noncubic_grid_and_tilings(monkeypatch, dtype, tile):
+    """Non-cubic grid with non-unit spacings; fp32 tiles of 256 lanes (two
+    units per tile row) and an untiled fp64 table."""
+    grid = GridSpec(12, 20, 7, 0.5, 0.25, 1.0 / 7)
+    dt = (DeviceTable.random(grid, 512, seed=2, tile_size=tile) if dtype == "f32"
+          else DeviceTable.normal_f64(grid, 128, seed=2, tile_size=tile))
+    pos = np.random.default_rng(12).random((9000, 3)) * np.array([6.0, 5.0, 1.0]) * 1.5 - 1.0
+    a, b = _both(monkeypatch, dt, "vgh", pos)
+    assert _eq(a, b)
