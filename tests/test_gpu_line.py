@@ -151,3 +151,17 @@ def test_line_noncubic_grid_and_tilings(monkeypatch, dtype, tile):
     pos = np.random.default_rng(12).random((9000, 3)) * np.array([6.0, 5.0, 1.0]) * 1.5 - 1.0
     a, b = _both(monkeypatch, dt, "vgh", pos)
     assert _eq(a, b)
+
+
+def test_line_edge_coordinates(monkeypatch):
+    """The reference's awkward coordinates (golden mapping set: +-0, denormals,
+    +-1e308, +-1e15, cell boundaries, negatives) through the line kernel."""
+    import os
+
+    xs = np.load(os.path.join(os.path.dirname(__file__), "golden", "mapping.npz"))["xs"]
+    grid = GridSpec(20, 24, 28, 0.05, 1 / 24, 1 / 28)
+    dt = DeviceTable.random(grid, 128, seed=4)
+    rng = np.random.default_rng(13)
+    pos = np.stack([rng.choice(xs, 20000), rng.choice(xs, 20000), rng.random(20000)], axis=1)
+    a, b = _both(monkeypatch, dt, "vgh", pos)
+    assert _eq(a, b)
