@@ -105,8 +105,9 @@ const char *spo_last_error(void);
  *           spo_eval_workspace_bytes(kind, dtype, mode, n_pos) bytes, 16-byte
  *           aligned, not shared with a concurrent call.  With it, FAST calls
  *           (fp32 and fp64) run the TMA-pipelined kernels: the line-window
- *           kernel for VGL/VGH batches of >= 1 position per grid cell (planes
- *           shared along grid lines), else the per-position kernel; with NULL
+ *           kernel for dense batches (VGL/VGH: >= 1 position per grid cell,
+ *           V: >= 2; planes shared along grid lines), else the per-position
+ *           kernel; with NULL
  *           they run the generic kernel.  Bitwise identical results either way
  *           (spo_eval_path tells which one runs).
  */
@@ -140,7 +141,7 @@ int spo_eval_lanes(int kind, int dtype, int mode, const void *table, const int32
  *   SPO_PATH_GENERIC  one-pass kernel (strict mode, no workspace, small batches)
  *   SPO_PATH_TMA      per-position TMA pipeline (spo_eval_tma.cu)
  *   SPO_PATH_LINE     line-window kernel: planes shared along grid lines, for
- *                     VGL/VGH batches of >= 1 position per grid cell
+ *                     VGL/VGH batches of >= 1 position per grid cell, V of >= 2
  *                     (spo_eval_line.cu)
  * -1 on bad arguments.  All paths give bitwise identical results.
  */

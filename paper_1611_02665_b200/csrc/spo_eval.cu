@@ -324,11 +324,11 @@ extern "C" int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64
     return a > b ? a : b;
 }
 
-// positions per grid cell from which the line-window kernel is used (NUM/DEN),
-// for VGL and VGH: sustained-rate crossover measured by
-// scripts/micro/line_sustained.py (V has too little math per plane to pay
-// for the plane-sharing protocol)
-constexpr long long LINE_DENSITY_NUM = 1, LINE_DENSITY_DEN = 1;
+// positions per grid cell from which the line-window kernel is used:
+// sustained-rate crossovers measured by scripts/micro/line_sustained.py and
+// scripts/bench_configs.py (V has little math per plane, so it needs more
+// sharing before the protocol pays: +15% at 2 positions per cell, -5% at 1)
+constexpr long long LINE_MIN_PER_CELL_VGX = 1, LINE_MIN_PER_CELL_V = 2;
 
 // line-window kernel for batches dense enough to share stencil planes along
 // grid lines (SPO_LINE=0/1 forces it off/on; read on every call)
@@ -336,7 +336,7 @@ static bool want_line(int kind, const int32_t *n3, long long n_pos) {
     const char *env_line = getenv("SPO_LINE");
     if (env_line) return env_line[0] == '1';
     const long long cells = (long long)n3[0] * n3[1] * n3[2];
-    return kind != SPO_KIND_V && n_pos * LINE_DENSITY_DEN >= cells * LINE_DENSITY_NUM;
+    return n_pos >= cells * (kind == SPO_KIND_V ? LINE_MIN_PER_CELL_V : LINE_MIN_PER_CELL_VGX);
 }
 
 // lane_limit < 0: every table lane is stored and `out` must be memory of the

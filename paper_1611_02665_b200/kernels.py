@@ -211,8 +211,9 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
     status     optional int32 CUDA tensor(1): set to 1 on a non-finite position
     check      raise DomainError for non-finite positions (one sync on status)
     pipeline   fast mode: True = the TMA-pipelined kernels (a workspace is
-               allocated here; the line-window kernel for VGL/VGH batches of
-               >= 1 position per grid cell, else the per-position kernel),
+               allocated here; the line-window kernel for dense batches --
+               VGL/VGH >= 1 position per grid cell, V >= 2 -- else the
+               per-position kernel),
                False = the generic kernel, "auto" = pipelined when
                P * lanes >= PIPELINE_MIN_WORK.  Same bits either way
                (eval_path() tells which kernel runs)

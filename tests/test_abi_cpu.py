@@ -93,7 +93,8 @@ def test_eval_path_selection(lib, monkeypatch):
     big = 1 << 40
     assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, big) == 2    # >= 1 position per cell: line
     assert lib.spo_eval_path(1, 0, 0, n3, 128, 32, 262144, big) == 2    # VGL too
-    assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 262144, big) == 1    # V: per-position TMA
+    assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 262144, big) == 1    # V below 2 per cell: TMA
+    assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 524288, big) == 2    # V at 2 per cell: line
     assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 200000, big) == 1    # sparser: per-position TMA
     assert lib.spo_eval_path(2, 0, 1, n3, 128, 32, 262144, big) == 0    # strict: generic
     assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, 0) == 0      # no workspace: generic
