@@ -50,6 +50,7 @@ constexpr int PLANE = 16 * ROWB;                 // bytes per plane slot
 constexpr int BPL = 64;                          // positions per item
 constexpr int PL = 4 * BPL + 4;                  // plane-list ints per run: count, planes, pad
 constexpr int PLB = PL * 4;                      // plane-list bytes per run (16-byte multiple)
+constexpr unsigned SPIN_NS = 256;                // back-off of the issued / release polls
 constexpr int PBATCH = 4;                        // planes issued together by the producer lanes
 constexpr int WS_HEADER = 1024;                  // ticket @0
 constexpr int NBK = 4;                           // spatial blocks per axis (as spo_eval_tma.cu)
@@ -337,6 +338,7 @@ __global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_cons
                         unsigned v = lane < CONSUMERS ? ld_acquire_shared(&relw[lane]) : 0xffffffffu;
                         v = __reduce_min_sync(0xffffffffu, v);
                         if (v >= need) break;
+                        __nanosleep(SPIN_NS);
                     }
                 }
                 const int t = t0 + lane;
@@ -431,8 +433,7 @@ __global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_cons
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const unsigned x = s0 + (unsigned)i;
-                while (ld_acquire_shared(issued) <= x) {
-                }
+                while (ld_acquire_shared(issued) <= x) __nanosleep(SPIN_NS);
                 const int sl = (int)(x % R);
                 mbar_wait(&full[sl], (x / R) & 1);
                 const T *p = reinterpret_cast<const T *>(planes + (size_t)sl * PLANE) + lane * W;
