@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0, help="positions per launch (0 = auto)")
     ap.add_argument("--mode", default="fast", choices=("fast", "strict"))
     ap.add_argument("--tile", type=int, default=-1, help="AoSoA tile size (-1 = auto, 0 = untiled)")
+    ap.add_argument("--form", default="auto", choices=("auto", "kpower", "bspline"),
+                    help="device table form of FAST evaluations (spo_b200.h SPO_TABLE_KPOWER); auto = "
+                         "k-power form for dense (line-kernel) batches")
     ap.add_argument("--walkers", type=int, default=0, help="override walkers per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu", action="store_true")
@@ -268,6 +271,9 @@ def run_b200(args):
     S = KernelKind(kind).output_streams_soa
     tile = "auto" if args.tile < 0 else (args.tile or None)
     table = DeviceTable.random(cfg.grid, N, seed=0, tile_size=tile, device=dev)
+    form = args.form if args.mode == "fast" else "bspline"
+    if form != "bspline":
+        table.with_kpower()
     pos = torch.from_numpy(pos_np).to(dev)
     chunk = args.chunk
     if chunk <= 0:  # largest of 2^19 / 2^18 whose output buffer leaves 40 GB free
@@ -283,7 +289,7 @@ def run_b200(args):
         for b, (lo, hi) in enumerate(bounds):
             if events is not None:
                 events[b][0].record(stream)
-            evaluate(table, kind, pos[lo:hi], out, mode=args.mode, check=False)
+            evaluate(table, kind, pos[lo:hi], out, mode=args.mode, check=False, form=form)
             if events is not None:
                 events[b][1].record(stream)
 
@@ -297,7 +303,7 @@ def run_b200(args):
 
     # correctness guard on the benchmarked configuration (one launch)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
-    evaluate(table, kind, pos[:chunk], out, mode=args.mode, status=status, check=False)
+    evaluate(table, kind, pos[:chunk], out, mode=args.mode, status=status, check=False, form=form)
     assert int(status.item()) == 0
 
     launch_events = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -330,21 +336,24 @@ def run_b200(args):
     total_units = P * N * args.steps * world
     value = total_units / (elapsed_ms / 1e3)
 
-    from paper_1611_02665_b200.kernels import eval_path
+    from paper_1611_02665_b200.kernels import eval_form, eval_path
 
-    path = eval_path(table, kind, chunk, mode=args.mode)
+    path = eval_path(table, kind, chunk, mode=args.mode, form=form)
+    form = eval_form(table, kind, chunk, mode=args.mode, form=form)  # the form the timed launches read
     # this repo's kernels per evaluate() call (library kernels -- cub's radix
     # sort in the line path's prologue, memsets -- not counted)
+    kp = "true" if form == "kpower" else "false"
     kernels_per_call, kernel_name = {
-        "line": (4, f"spo::line::line_kernel<{kind.upper()},float> (+ line_keys, cub sort, line_records, "
-                    f"line_runs prologue, timed together)"),
-        "tma": (3, f"spo::tma::eval_tma_kernel<{kind.upper()}> (+ bucket_count, prologue_records, timed together)"),
-        "generic": (1, f"spo::eval_kernel<{kind.upper()},float,{args.mode}>"),
+        "line": (4, f"spo::line::line_kernel<{kind.upper()},float,RATIO=false,KP={kp}> (+ line_keys, cub sort, "
+                    f"line_records, line_runs prologue, timed together)"),
+        "tma": (3, f"spo::tma::eval_tma_kernel<{kind.upper()},KP={kp}> (+ bucket_count, prologue_records, "
+                   f"timed together)"),
+        "generic": (1, f"spo::eval_kernel<{kind.upper()},float,{args.mode},KP={kp}>"),
     }[path]
     peak, peak_src = measured_peak()
     achieved = bpp * chunk / (avg_launch_ms * 1e-3) / 1e9  # GB/s per launch
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(args, cfg, kind, chunk, path),
+                "frac": achieved / peak, "traffic": ncu_traffic(args, cfg, kind, chunk, path, form),
                 "peak_source": peak_src, "kernel": kernel_name,
                 "algorithmic_bytes_per_position": bpp, "positions_per_launch": chunk,
                 "avg_launch_ms": avg_launch_ms}
@@ -359,7 +368,8 @@ def run_b200(args):
         "config": {"workload": f"cfg{cfg.index}: {cfg.description}", "grid": list(cfg.grid.counts),
                    "n_splines": N, "kernel": kind, "positions_per_gpu": P, "walkers_per_gpu": P // cfg.moves,
                    "chunk": chunk, "mode": args.mode, "path": path, "tile_size": table.tile_size,
-                   "table_gb": table.nbytes / 1e9,
+                   "table_gb": table.nbytes / 1e9, "table_form": form,
+                   "kpower_table_gb": (table.kdata.numel() * 4 / 1e9) if table.has_kpower else None,
                    "l2": f"inputs larger than L2 (table {table.nbytes / 1e9:.2f} GB >> 126 MB); no flush",
                    "parallelism": f"walker-sharded x{world}, table replicated"},
         "roofline": roofline,
@@ -452,13 +462,15 @@ def e2e_dropin(table, kind, pos_np, N, S, eval_batch, WalkerOutputsSoA, args, de
             "api": "paper_1611_02665_b200.eval_batch(table, kind, host positions, host WalkerOutputsSoA)"}
 
 
-def ncu_traffic(args, cfg, kind, chunk, path):
+def ncu_traffic(args, cfg, kind, chunk, path, form="bspline"):
     """dram read+write bytes per launch from the committed ncu capture, when
     it was taken on this exact configuration (profiles/ncu_traffic.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             rec = json.load(f)
         key = f"cfg{cfg.index}-{kind}-{args.mode}-tile{args.tile}-{path}-{chunk}"
+        if form == "kpower":
+            key += "-kpower"
         r = rec.get(key)
         if r and r.get("positions_per_launch") == chunk:
             return r["dram_bytes_per_launch"]

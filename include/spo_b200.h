@@ -17,6 +17,9 @@
  *                   map_to_grid / basis_weights (grid.py:155-213) and the
  *                   bit-exact index tests.
  *   spo_basis_weights  replaces grid.py:180-203 (basis_weights[_batch]).
+ *   spo_pack_kpower  beyond the reference: the k-power form of a device
+ *                   table (z-cubics in the power basis, SPO_TABLE_KPOWER),
+ *                   the FAST kernels' cheaper table form.
  *   spo_pack_table  replaces the host table layout of coeffs.py:117-138 /
  *                   141-158 (+ tile_table 197-210): uploads a reference SoA
  *                   table into the device's wrap-padded AoSoA layout.
@@ -66,7 +69,7 @@
 extern "C" {
 #endif
 
-#define SPO_ABI_VERSION 5
+#define SPO_ABI_VERSION 6
 
 /* kernel kinds: KernelKind (kernels.py:26-51) */
 #define SPO_KIND_V 0
@@ -81,6 +84,20 @@ extern "C" {
 #define SPO_MODE_FAST 0   /* separable FMA accumulation (k, then j, then i)        */
 #define SPO_MODE_STRICT 1 /* reference order, fp32 mul then add, no FMA: bitwise
                              equal to kernels.py:143-247                         */
+/*
+ * Table-form flag, OR-ed into `mode` (FAST only): `table` is in the k-power
+ * form built by spo_pack_kpower -- per (m, i', j') the rows 4*k0 + r, r < 4,
+ * hold the power-basis coefficients of the z-cubic of cell k0,
+ *   q0 = (c0 + 4 c1 + c2)/6, q1 = (c2 - c0)/2, q2 = (c0 - 2 c1 + c2)/2,
+ *   q3 = (c3 - c0)/6 + (c1 - c2)/2      (c_r = B-spline row k0 + r),
+ * so sum_k a_k(t) c_k = q0 + t q1 + t^2 q2 + t^3 q3 for the basis of
+ * grid.py:127-130.  The z-sums then cost 7 FMAs per row group instead of 12
+ * (VGH: 248 instead of 328 FMAs per orbital); the table is 4 nz / (nz + 3)
+ * times larger.  Results are within the FAST tolerance of the oracle, not
+ * bitwise equal to the B-spline form (every path is bitwise equal to every
+ * other path on the same form).
+ */
+#define SPO_TABLE_KPOWER 0x100
 
 /* return codes */
 #define SPO_OK 0
@@ -195,6 +212,15 @@ int spo_basis_weights(int dtype, const double *t, int64_t n, double dinv, double
 int spo_pack_table(int dtype, const void *src, int32_t src_npad, int32_t n_splines,
                    const int32_t *n3, int32_t tile_size, int32_t nb, int32_t n_tiles, void *dst,
                    void *stream);
+
+/*
+ * Build the k-power form (see SPO_TABLE_KPOWER) of a device table `src` in
+ * the B-spline layout above: dst[m][i'][j'][4*k0 + r][l], i' < nx+3, j' < ny+3,
+ * k0 < nz, r < 4, computed in fp64 and rounded once to the table dtype.  Same
+ * tiling (nb, n_tiles) as src; dst holds n_tiles*(nx+3)*(ny+3)*4nz*nb elements.
+ */
+int spo_pack_kpower(int dtype, const void *src, const int32_t *n3, int32_t nb, int32_t n_tiles, void *dst,
+                    void *stream);
 
 /*
  * Fill the device layout with FillSpec.random(seed) values: spline n uses the

@@ -18,13 +18,14 @@ LIB_PATH = os.path.join(_PKG, "libspo_b200.so")
 KIND_V, KIND_VGL, KIND_VGH = 0, 1, 2
 F32, F64 = 0, 1
 MODE_FAST, MODE_STRICT = 0, 1
-ABI_VERSION = 5
+TABLE_KPOWER = 0x100  # OR-ed into the mode: the table is in the k-power form
+ABI_VERSION = 6
 
 EXPORTS = ("spo_abi_version", "spo_last_error", "spo_eval", "spo_eval_lanes", "spo_eval_path",
            "spo_eval_workspace_bytes",
            "spo_eval_ratios", "spo_eval_ratios_workspace_bytes", "spo_prologue",
            "spo_basis_weights",
-           "spo_pack_table",
+           "spo_pack_table", "spo_pack_kpower",
            "spo_fill_uniform", "spo_fill_normal_f64", "spo_fill_positions")
 
 _lock = threading.Lock()
@@ -74,6 +75,8 @@ def load(build_if_missing: bool = True):
         L.spo_basis_weights.argtypes = [ip, vp, i64, dbl, dbl, vp, vp]
         L.spo_pack_table.restype = ip
         L.spo_pack_table.argtypes = [ip, vp, i32, i32, P(i32), i32, i32, i32, vp, vp]
+        L.spo_pack_kpower.restype = ip
+        L.spo_pack_kpower.argtypes = [ip, vp, P(i32), i32, i32, vp, vp]
         L.spo_fill_uniform.restype = ip
         L.spo_fill_uniform.argtypes = [vp, i32, P(i32), i32, i32, i32, vp, vp]
         L.spo_fill_normal_f64.restype = ip

@@ -110,15 +110,20 @@ inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 
 inline int dtype_size(int dtype) { return dtype == SPO_F64 ? 8 : 4; }
 
 // Device table geometry shared by the eval, pack and fill kernels.
+// B-spline form: rows k' < nz + 3 per (i', j'), the stencil of cell k0 is
+// rows k0..k0+3.  k-power form (SPO_TABLE_KPOWER): rows 4*k0 + r (r < 4) hold
+// the power-basis coefficients q_r of cell k0 along z, nzp = 4 nz, kmul = 4.
 struct TableGeom {
     int nx, ny, nz;        // reference grid counts
-    int nxp, nyp, nzp;     // wrap-padded counts (n + 3)
+    int nxp, nyp, nzp;     // wrap-padded counts (n + 3); k-power: nzp = 4 nz
     int nb;                // row length (lanes) per tile
     int n_tiles;
     long long tile_stride; // elements per tile
+    int kmul;              // row of cell k0's first stencil row = kmul * k0
 };
 
-inline int make_geom(const int32_t *n3, int32_t nb, int32_t n_tiles, int dtype, TableGeom *g) {
+inline int make_geom(const int32_t *n3, int32_t nb, int32_t n_tiles, int dtype, TableGeom *g,
+                     bool kpower = false) {
     if (!n3) return fail(SPO_ERR_CONTRACT, "grid counts pointer is NULL");
     for (int a = 0; a < 3; ++a)
         if (n3[a] < 4) return fail(SPO_ERR_CONFIG, "grid count %d on axis %d must be >= 4", n3[a], a);
@@ -132,7 +137,8 @@ inline int make_geom(const int32_t *n3, int32_t nb, int32_t n_tiles, int dtype, 
     g->nz = n3[2];
     g->nxp = n3[0] + 3;
     g->nyp = n3[1] + 3;
-    g->nzp = n3[2] + 3;
+    g->nzp = kpower ? 4 * n3[2] : n3[2] + 3;
+    g->kmul = kpower ? 4 : 1;
     g->nb = nb;
     g->n_tiles = n_tiles;
     g->tile_stride = (long long)g->nxp * g->nyp * g->nzp * nb;

@@ -62,6 +62,10 @@ __device__ __forceinline__ void st16(double *p, const double *r) {
 }
 __device__ __forceinline__ float fmaT(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ double fmaT(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float addT(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double addT(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float mulT(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mulT(double a, double b) { return __dmul_rn(a, b); }
 
 template <int KIND>
 struct Streams {
@@ -85,12 +89,18 @@ struct EvalArgs {
     const long long *out_index;
     long long lane_limit;  // output lanes >= lane_limit are not stored
     int *status;
+    int kmul;              // k-power tables: cell k0's rows start at 4 k0
+    double dz, dz2;        // k-power tables: 1/dz, 2/dz^2
 };
 
 // ---------------------------------------------------------------- FAST ----
-template <int KIND, typename T>
+//   KP     k-power tables (spo_b200.h SPO_TABLE_KPOWER): the four rows are the
+//          power-basis q0..q3 of the z-cubic; A, D, H as spo_tma.cuh kpow_sums
+//          (w[24] = t_z), 1/dz and 2/dz^2 folded into the x weights -- the
+//          sequence of the TMA and line kernels' slab_contract_kp (bitwise).
+template <int KIND, typename T, bool KP>
 __device__ __forceinline__ void contract_fast(const T *__restrict__ rp, long long si, long long sj,
-                                              long long sk, const T *__restrict__ w,
+                                              long long sk, const T *__restrict__ w, T dz, T dz2,
                                               T (&acc)[Streams<KIND>::S][Vec<T>::W]) {
     constexpr int W = Vec<T>::W;
     T wx[12], wy[12], wz[12];
@@ -121,13 +131,25 @@ __device__ __forceinline__ void contract_fast(const T *__restrict__ rp, long lon
             ld16(r + 3 * sk, c3);
 #pragma unroll
             for (int e = 0; e < W; ++e) {
-                const T s0 = fmaT(wz[3], c3[e], fmaT(wz[2], c2[e], fmaT(wz[1], c1[e], wz[0] * c0[e])));
+                T s0, s1, s2;
+                if constexpr (KP) {
+                    const T tz = wz[0];
+                    const T q = fmaT(tz, c3[e], c2[e]);  // q2 + t q3
+                    s0 = fmaT(tz, fmaT(tz, q, c1[e]), c0[e]);
+                    if (KIND != SPO_KIND_V) {
+                        const T h = fmaT(tz, c3[e], q);  // q2 + 2t q3
+                        s1 = fmaT(tz, addT(q, h), c1[e]);
+                        s2 = fmaT(tz, c3[e], h);
+                    }
+                } else {
+                    s0 = fmaT(wz[3], c3[e], fmaT(wz[2], c2[e], fmaT(wz[1], c1[e], wz[0] * c0[e])));
+                    if (KIND != SPO_KIND_V) {
+                        s1 = fmaT(wz[7], c3[e], fmaT(wz[6], c2[e], fmaT(wz[5], c1[e], wz[4] * c0[e])));
+                        s2 = fmaT(wz[11], c3[e], fmaT(wz[10], c2[e], fmaT(wz[9], c1[e], wz[8] * c0[e])));
+                    }
+                }
                 t00[e] = fmaT(wy[j], s0, t00[e]);
                 if (KIND != SPO_KIND_V) {
-                    const T s1 =
-                        fmaT(wz[7], c3[e], fmaT(wz[6], c2[e], fmaT(wz[5], c1[e], wz[4] * c0[e])));
-                    const T s2 =
-                        fmaT(wz[11], c3[e], fmaT(wz[10], c2[e], fmaT(wz[9], c1[e], wz[8] * c0[e])));
                     t10[e] = fmaT(wy[4 + j], s0, t10[e]);
                     t01[e] = fmaT(wy[j], s1, t01[e]);
                     t20[e] = fmaT(wy[8 + j], s0, t20[e]);
@@ -137,24 +159,29 @@ __device__ __forceinline__ void contract_fast(const T *__restrict__ rp, long lon
             }
         }
 #pragma unroll
+        // z-derivative x weights: the B-spline form carries 1/dz in wz; the
+        // k-power form folds it here (axz = ax/dz, daxz = dax/dz, axz2 = 2ax/dz^2)
+        const T axz = KP ? mulT(wx[i], dz) : wx[i], daxz = KP ? mulT(wx[4 + i], dz) : wx[4 + i];
+        const T axz2 = KP ? mulT(wx[i], dz2) : wx[i];
+#pragma unroll
         for (int e = 0; e < W; ++e) {
             acc[0][e] = fmaT(wx[i], t00[e], acc[0][e]);
             if (KIND != SPO_KIND_V) {
                 acc[1][e] = fmaT(wx[4 + i], t00[e], acc[1][e]);  // gx
                 acc[2][e] = fmaT(wx[i], t10[e], acc[2][e]);      // gy
-                acc[3][e] = fmaT(wx[i], t01[e], acc[3][e]);      // gz
+                acc[3][e] = fmaT(axz, t01[e], acc[3][e]);        // gz
             }
             if (KIND == SPO_KIND_VGL) {
                 // l = d2x*t00 + x*t20 + x*t02
-                acc[4][e] = fmaT(wx[8 + i], t00[e], fmaT(wx[i], t20[e], fmaT(wx[i], t02[e], acc[4][e])));
+                acc[4][e] = fmaT(wx[8 + i], t00[e], fmaT(wx[i], t20[e], fmaT(axz2, t02[e], acc[4][e])));
             }
             if (KIND == SPO_KIND_VGH) {
                 acc[4][e] = fmaT(wx[8 + i], t00[e], acc[4][e]);  // hxx
                 acc[5][e] = fmaT(wx[4 + i], t10[e], acc[5][e]);  // hxy
-                acc[6][e] = fmaT(wx[4 + i], t01[e], acc[6][e]);  // hxz
+                acc[6][e] = fmaT(daxz, t01[e], acc[6][e]);       // hxz
                 acc[7][e] = fmaT(wx[i], t20[e], acc[7][e]);      // hyy
-                acc[8][e] = fmaT(wx[i], t11[e], acc[8][e]);      // hyz
-                acc[9][e] = fmaT(wx[i], t02[e], acc[9][e]);      // hzz
+                acc[8][e] = fmaT(axz, t11[e], acc[8][e]);        // hyz
+                acc[9][e] = fmaT(axz2, t02[e], acc[9][e]);       // hzz
             }
         }
     }
@@ -221,7 +248,7 @@ __device__ __forceinline__ void contract_strict(const float *__restrict__ rp, lo
 }
 
 // -------------------------------------------------------------- kernel ----
-template <int KIND, typename T, bool STRICT>
+template <int KIND, typename T, bool STRICT, bool KP>
 __global__ void __launch_bounds__(256, 1) eval_kernel(const EvalArgs a) {
     constexpr int W = Vec<T>::W;
     constexpr int S = Streams<KIND>::S;
@@ -244,8 +271,9 @@ __global__ void __launch_bounds__(256, 1) eval_kernel(const EvalArgs a) {
         axis_weights<T>(tx, a.g.dinv[0], a.g.delta[0], sw + q * 36);
         axis_weights<T>(ty, a.g.dinv[1], a.g.delta[1], sw + q * 36 + 12);
         axis_weights<T>(tz, a.g.dinv[2], a.g.delta[2], sw + q * 36 + 24);
+        if (KP) sw[q * 36 + 24] = (T)tz;
         const bool finite = isfinite(x) && isfinite(y) && isfinite(z);
-        sbase[q] = finite ? ((long long)i0 * a.nyp + j0) * a.nzp * a.nb + (long long)k0 * a.nb : -1;
+        sbase[q] = finite ? ((long long)i0 * a.nyp + j0) * a.nzp * a.nb + (long long)k0 * a.kmul * a.nb : -1;
         if (!finite && a.status) atomicOr(a.status, 1);
     }
     __syncthreads();
@@ -263,7 +291,7 @@ __global__ void __launch_bounds__(256, 1) eval_kernel(const EvalArgs a) {
             if constexpr (STRICT) {
                 contract_strict<KIND>(tb + base, a.si, a.sj, a.sk, sw + q * 36, acc);
             } else {
-                contract_fast<KIND, T>(tb + base, a.si, a.sj, a.sk, sw + q * 36, acc);
+                contract_fast<KIND, T, KP>(tb + base, a.si, a.sj, a.sk, sw + q * 36, (T)a.dz, (T)a.dz2, acc);
             }
         } else {
 #pragma unroll
@@ -287,9 +315,9 @@ __global__ void __launch_bounds__(256, 1) eval_kernel(const EvalArgs a) {
     }
 }
 
-template <int KIND, typename T, bool STRICT>
+template <int KIND, typename T, bool STRICT, bool KP = false>
 static int launch(const EvalArgs &a, dim3 grid, dim3 block, size_t smem, cudaStream_t st) {
-    eval_kernel<KIND, T, STRICT><<<grid, block, smem, st>>>(a);
+    eval_kernel<KIND, T, STRICT, KP><<<grid, block, smem, st>>>(a);
     return check_launch("spo_eval launch");
 }
 
@@ -319,6 +347,7 @@ extern "C" const char *spo_last_error(void) { return last_error_slot().c_str(); 
 
 extern "C" int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64_t n_pos) {
     if (kind < SPO_KIND_V || kind > SPO_KIND_VGH || n_pos < 0) return -1;
+    mode &= ~SPO_TABLE_KPOWER;
     if ((dtype != SPO_F32 && dtype != SPO_F64) || mode != SPO_MODE_FAST) return 0;
     const long long a = eval_tma_workspace_bytes(dtype, n_pos), b = eval_line_workspace_bytes(dtype, n_pos);
     return a > b ? a : b;
@@ -350,11 +379,15 @@ static int eval_impl(int kind, int dtype, int mode, const void *table, const int
                      void *stream) {
     if (kind < SPO_KIND_V || kind > SPO_KIND_VGH) return fail(SPO_ERR_CONTRACT, "unknown kind %d", kind);
     if (dtype != SPO_F32 && dtype != SPO_F64) return fail(SPO_ERR_CONTRACT, "unknown dtype %d", dtype);
+    const bool kpower = (mode & SPO_TABLE_KPOWER) != 0;
+    mode &= ~SPO_TABLE_KPOWER;
     if (mode != SPO_MODE_FAST && mode != SPO_MODE_STRICT) return fail(SPO_ERR_CONTRACT, "unknown mode %d", mode);
     if (mode == SPO_MODE_STRICT && dtype != SPO_F32)
         return fail(SPO_ERR_CONFIG, "strict mode reproduces the fp32 reference kernels only");
+    if (mode == SPO_MODE_STRICT && kpower)
+        return fail(SPO_ERR_CONFIG, "strict mode needs the B-spline table form (the reference's arithmetic)");
     TableGeom geo;
-    int rc = make_geom(n3, nb, n_tiles, dtype, &geo);
+    int rc = make_geom(n3, nb, n_tiles, dtype, &geo, kpower);
     if (rc) return rc;
     if (n_pos < 0) return fail(SPO_ERR_CONTRACT, "n_pos=%lld < 0", (long long)n_pos);
     if (n_pos == 0) return ok();
@@ -441,6 +474,9 @@ static int eval_impl(int kind, int dtype, int mode, const void *table, const int
     a.out_index = reinterpret_cast<const long long *>(out_index);
     a.lane_limit = lanes;
     a.status = status;
+    a.kmul = geo.kmul;
+    a.dz = dinv3[2];
+    a.dz2 = 2.0 * dinv3[2] * dinv3[2];
 
     const int groups = 256 / chv;
     const long long n_chunks = (long long)a.chunks_per_tile * n_tiles;
@@ -457,6 +493,20 @@ static int eval_impl(int kind, int dtype, int mode, const void *table, const int
     const size_t smem = (size_t)a.ppc * (36 * (size_t)(dtype == SPO_F64 ? 8 : 4) + 8);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
 
+    if (kpower) {
+        if (dtype == SPO_F64) {
+            switch (kind) {
+                case SPO_KIND_V: return launch<SPO_KIND_V, double, false, true>(a, grid, block, smem, st);
+                case SPO_KIND_VGL: return launch<SPO_KIND_VGL, double, false, true>(a, grid, block, smem, st);
+                default: return launch<SPO_KIND_VGH, double, false, true>(a, grid, block, smem, st);
+            }
+        }
+        switch (kind) {
+            case SPO_KIND_V: return launch<SPO_KIND_V, float, false, true>(a, grid, block, smem, st);
+            case SPO_KIND_VGL: return launch<SPO_KIND_VGL, float, false, true>(a, grid, block, smem, st);
+            default: return launch<SPO_KIND_VGH, float, false, true>(a, grid, block, smem, st);
+        }
+    }
     if (dtype == SPO_F64) {
         switch (kind) {
             case SPO_KIND_V: return launch<SPO_KIND_V, double, false>(a, grid, block, smem, st);
@@ -481,8 +531,11 @@ static int eval_impl(int kind, int dtype, int mode, const void *table, const int
 extern "C" int spo_eval_path(int kind, int dtype, int mode, const int32_t *n3, int32_t nb, int32_t n_tiles,
                              int64_t n_pos, int64_t workspace_bytes) {
     if (kind < SPO_KIND_V || kind > SPO_KIND_VGH || (dtype != SPO_F32 && dtype != SPO_F64) || n_pos < 0) return -1;
+    const bool kpower = (mode & SPO_TABLE_KPOWER) != 0;
+    mode &= ~SPO_TABLE_KPOWER;
+    if (kpower && mode != SPO_MODE_FAST) return -1;
     TableGeom geo;
-    if (make_geom(n3, nb, n_tiles, dtype, &geo)) return -1;
+    if (make_geom(n3, nb, n_tiles, dtype, &geo, kpower)) return -1;
     if (mode != SPO_MODE_FAST || workspace_bytes <= 0) return SPO_PATH_GENERIC;
     const char *env_tma = getenv("SPO_TMA");
     if (env_tma && env_tma[0] == '0') return SPO_PATH_GENERIC;

@@ -115,6 +115,10 @@ struct LArgs {
     const void *coef;           // [n_pos][coef_stride] in output-lane layout
     long long coef_stride;
     double *partials;           // [units][n_pos][S]
+    // k-power tables (KP kernels): TMA row coordinate = kmul * k0 (4: four
+    // power-basis rows per cell), z-derivative factors 1/dz and 2/dz^2
+    int kmul;
+    double dz, dz2;
 };
 
 struct LItem {
@@ -146,7 +150,7 @@ __global__ void line_keys_kernel(GridArgs g, const double *__restrict__ pos, lon
 
 template <typename T>
 __global__ void line_records_kernel(GridArgs g, const double *__restrict__ pos, const int *__restrict__ order,
-                                    long long n, unsigned char *__restrict__ recs) {
+                                    long long n, unsigned char *__restrict__ recs, int kpower) {
     constexpr int RECB = LT<T>::RECB;
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
          q += (long long)gridDim.x * blockDim.x) {
@@ -160,6 +164,7 @@ __global__ void line_records_kernel(GridArgs g, const double *__restrict__ pos, 
         axis_weights<T>(tx, g.dinv[0], g.delta[0], w);
         axis_weights<T>(ty, g.dinv[1], g.delta[1], w + 12);
         axis_weights<T>(tz, g.dinv[2], g.delta[2], w + 24);
+        if (kpower) w[24] = (T)tz;  // k-power tables: the z weight is t itself
         if (!(isfinite(x) && isfinite(y) && isfinite(z))) i0 = -1;
         unsigned char *dst = recs + q * RECB;
 #pragma unroll
@@ -230,7 +235,7 @@ static_assert(smem_bytes<float>() <= 232448, "shared memory budget");
 static_assert(smem_bytes<double>() <= 232448, "shared memory budget");
 
 // ---------------------------------------------------------------- kernel --
-template <int KIND, typename T, bool RATIO>
+template <int KIND, typename T, bool RATIO, bool KP>
 __global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_constant__ CUtensorMap tmap, const LArgs a) {
     constexpr int S = NS<KIND>::S;
     constexpr int CONSUMERS = cons_warps<T>();
@@ -351,7 +356,7 @@ __global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_cons
                     if (n > 0) mbar_wait(&full[sl], (n - 1) & 1);
                     const int c = pl[1 + t];
                     mbar_arrive_expect_tx(&full[sl], PLANE);
-                    tma_load_5d(planes + (size_t)sl * PLANE, &tmap, &full[sl], lt, (c >> 20) & 0x3ff,
+                    tma_load_5d(planes + (size_t)sl * PLANE, &tmap, &full[sl], lt, a.kmul * ((c >> 20) & 0x3ff),
                                 (c >> 10) & 0x3ff, c & 0x3ff, tile, policy);
                 }
                 __syncwarp();
@@ -423,7 +428,7 @@ __global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_cons
             }
             const unsigned s0 = base + (unsigned)(cell.z & 0xffff);
             const T *w = reinterpret_cast<const T *>(rec);
-            T wx[12], wy[12], wz[12];
+            T wx[12], wy[12], wz[12];  // k-power tables: wz[0] = t_z, the rest unused
 #pragma unroll
             for (int e = 0; e < 12; ++e) {
                 wx[e] = w[e];
@@ -437,7 +442,13 @@ __global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_cons
                 const int sl = (int)(x % R);
                 mbar_wait(&full[sl], (x / R) & 1);
                 const T *p = reinterpret_cast<const T *>(planes + (size_t)sl * PLANE) + lane * W;
-                slab_contract<KIND, BOXL>(p, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
+                if constexpr (KP) {
+                    const T dz = (T)a.dz, dz2 = (T)a.dz2;
+                    slab_contract_kp<KIND, BOXL>(p, wy, wz[0], wx[i], wx[4 + i], wx[8 + i], mul_rn(wx[i], dz),
+                                                 mul_rn(wx[4 + i], dz), mul_rn(wx[i], dz2), acc);
+                } else {
+                    slab_contract<KIND, BOXL>(p, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
+                }
             }
             publish(first_plane(q + CONSUMERS));  // this position's planes are read
             if constexpr (RATIO) {
@@ -463,18 +474,19 @@ __global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_cons
     }
 }
 
-template <int KIND, typename T, bool RATIO>
+template <int KIND, typename T, bool RATIO, bool KP>
 static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
     constexpr size_t sm = smem_bytes<T>();
     int grid = (int)min((long long)sms, a.n_items);
     if (grid < 1) grid = 1;
-    cudaFuncSetAttribute(line_kernel<KIND, T, RATIO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    line_kernel<KIND, T, RATIO><<<grid, threads<T>(), sm, st>>>(map, a);
+    cudaFuncSetAttribute(line_kernel<KIND, T, RATIO, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    line_kernel<KIND, T, RATIO, KP><<<grid, threads<T>(), sm, st>>>(map, a);
     return check_launch("spo_eval (line) launch");
 }
 template <int KIND, typename T>
-static int launch_r(bool ratio, const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
-    return ratio ? launch<KIND, T, true>(map, a, sms, st) : launch<KIND, T, false>(map, a, sms, st);
+static int launch_r(bool ratio, bool kp, const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
+    if (kp) return ratio ? launch<KIND, T, true, true>(map, a, sms, st) : launch<KIND, T, false, true>(map, a, sms, st);
+    return ratio ? launch<KIND, T, true, false>(map, a, sms, st) : launch<KIND, T, false, false>(map, a, sms, st);
 }
 
 static size_t pad256(size_t b) { return (b + 255) / 256 * 256; }
@@ -564,10 +576,10 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     const int *order = vals.Current();  // the sorted original indices (either buffer)
     const unsigned run_blocks = (unsigned)((n_pos + (long long)BPL * 128 - 1) / ((long long)BPL * 128));
     if (dtype == SPO_F64) {
-        line_records_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(g, pos, order, n_pos, recs);
+        line_records_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(g, pos, order, n_pos, recs, geo.kmul != 1);
         line_runs_kernel<double><<<run_blocks, 128, 0, st>>>(n_pos, recs, plist);
     } else {
-        line_records_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(g, pos, order, n_pos, recs);
+        line_records_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(g, pos, order, n_pos, recs, geo.kmul != 1);
         line_runs_kernel<float><<<run_blocks, 128, 0, st>>>(n_pos, recs, plist);
     }
     int rc = check_launch("spo_eval (line prologue)");
@@ -593,18 +605,22 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     a.coef = coef;
     a.coef_stride = coef_stride;
     a.partials = ratio ? reinterpret_cast<double *>(ws + eval_line_workspace_bytes(dtype, n_pos)) : nullptr;
+    const bool kp = geo.kmul != 1;
+    a.kmul = geo.kmul;
+    a.dz = g.dinv[2];
+    a.dz2 = 2.0 * g.dinv[2] * g.dinv[2];
 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (dtype == SPO_F64)
-        rc = kind == SPO_KIND_V     ? launch_r<SPO_KIND_V, double>(ratio, map, a, sms, st)
-             : kind == SPO_KIND_VGL ? launch_r<SPO_KIND_VGL, double>(ratio, map, a, sms, st)
-                                    : launch_r<SPO_KIND_VGH, double>(ratio, map, a, sms, st);
+        rc = kind == SPO_KIND_V     ? launch_r<SPO_KIND_V, double>(ratio, kp, map, a, sms, st)
+             : kind == SPO_KIND_VGL ? launch_r<SPO_KIND_VGL, double>(ratio, kp, map, a, sms, st)
+                                    : launch_r<SPO_KIND_VGH, double>(ratio, kp, map, a, sms, st);
     else
-        rc = kind == SPO_KIND_V     ? launch_r<SPO_KIND_V, float>(ratio, map, a, sms, st)
-             : kind == SPO_KIND_VGL ? launch_r<SPO_KIND_VGL, float>(ratio, map, a, sms, st)
-                                    : launch_r<SPO_KIND_VGH, float>(ratio, map, a, sms, st);
+        rc = kind == SPO_KIND_V     ? launch_r<SPO_KIND_V, float>(ratio, kp, map, a, sms, st)
+             : kind == SPO_KIND_VGL ? launch_r<SPO_KIND_VGL, float>(ratio, kp, map, a, sms, st)
+                                    : launch_r<SPO_KIND_VGH, float>(ratio, kp, map, a, sms, st);
     if (rc || !ratio) return rc;
     return ratio_reduce(kind, a.partials, units, n_pos, ratios, st);
 }

@@ -81,6 +81,8 @@ struct Args {
     const void *coef;           // [n_pos][coef_stride] in output-lane layout, pad lanes 0
     long long coef_stride;
     double *partials;           // [units][n_pos][S]
+    int kmul;                   // k-power tables: cell k0's rows start at 4 k0
+    double dz, dz2;             // k-power tables: 1/dz, 2/dz^2
 };
 
 // ------------------------------------------------------------ prologue --
@@ -136,7 +138,7 @@ template <typename T>
 __global__ void prologue_records_kernel(GridArgs g, const double *__restrict__ pos, long long n,
                                         const unsigned char *__restrict__ bucket,
                                         const unsigned *__restrict__ counts, unsigned *__restrict__ cursors,
-                                        unsigned char *__restrict__ recs, int *__restrict__ status) {
+                                        unsigned char *__restrict__ recs, int *__restrict__ status, int kpower) {
     constexpr int RECB = TT<T>::RECB;
     __shared__ unsigned offs[NBUCKET], local[NBUCKET], base[NBUCKET];
     if (threadIdx.x == 0) {
@@ -166,6 +168,7 @@ __global__ void prologue_records_kernel(GridArgs g, const double *__restrict__ p
             axis_weights<T>(tx, g.dinv[0], g.delta[0], w);
             axis_weights<T>(ty, g.dinv[1], g.delta[1], w + 12);
             axis_weights<T>(tz, g.dinv[2], g.delta[2], w + 24);
+            if (kpower) w[24] = (T)tz;  // k-power tables: the z weight is t itself
             if (!(isfinite(x) && isfinite(y) && isfinite(z))) {
                 if (status) atomicOr(status, 1);
                 i0 = -1;
@@ -193,7 +196,7 @@ struct GroupDesc {
     int c0, m;
 };
 
-template <int KIND, typename T, int CW, class C, bool RATIO>
+template <int KIND, typename T, int CW, class C, bool RATIO, bool KP>
 __global__ void __launch_bounds__(C::WARPS * 32, 1)
     eval_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Args a) {
     constexpr int WARPS = C::WARPS, BP = C::BP;
@@ -266,7 +269,7 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
             const bool ok = p < it.nb && cell.x >= 0;
             d.x[q] = ok ? cell.x : -1;
             d.y[q] = cell.y;
-            d.z[q] = cell.z;
+            d.z[q] = cell.z * a.kmul;
             d.bytes += ok ? SLAB : 0;
         }
     };
@@ -358,7 +361,13 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
                     ph0 ^= 1;
                 }
                 const T *slab = reinterpret_cast<const T *>(ring + st * STAGE + pp * SLAB) + vl * W;
-                slab_contract<KIND, CW>(slab, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
+                if constexpr (KP) {
+                    const T dz = (T)a.dz, dz2 = (T)a.dz2;
+                    slab_contract_kp<KIND, CW>(slab, wy, wz[0], wx[i], wx[4 + i], wx[8 + i], mul_rn(wx[i], dz),
+                                               mul_rn(wx[4 + i], dz), mul_rn(wx[i], dz2), acc);
+                } else {
+                    slab_contract<KIND, CW>(slab, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
+                }
                 st ^= 1;
             }
             if constexpr (RATIO) {
@@ -403,15 +412,15 @@ constexpr size_t smem_bytes() {
 static_assert(smem_bytes<float>() <= 232448, "shared memory budget");
 static_assert(smem_bytes<double>() <= 232448, "shared memory budget");
 
-template <int KIND, typename T, int CW, bool RATIO>
+template <int KIND, typename T, int CW, bool RATIO, bool KP = false>
 static int launch_t(const CUtensorMap &map, const Args &a, int sms, cudaStream_t st) {
     using C = typename TT<T>::Cfg;
     constexpr size_t sm = smem_bytes<T>();
     int grid = (int)min((long long)sms, (a.n_items + C::WARPS - 1) / C::WARPS);
     if (grid < 1) grid = 1;
-    cudaFuncSetAttribute(eval_tma_kernel<KIND, T, CW, C, RATIO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(eval_tma_kernel<KIND, T, CW, C, RATIO, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
-    eval_tma_kernel<KIND, T, CW, C, RATIO><<<grid, C::WARPS * 32, sm, st>>>(map, a);
+    eval_tma_kernel<KIND, T, CW, C, RATIO, KP><<<grid, C::WARPS * 32, sm, st>>>(map, a);
     return check_launch("spo_eval (tma) launch");
 }
 
@@ -421,6 +430,13 @@ template <int KIND, typename T>
 static int launch_cw(int cw_bytes, bool ratio, const CUtensorMap &map, const Args &a, int sms, cudaStream_t st) {
     constexpr int E = (int)sizeof(T);
     if (ratio) return launch_t<KIND, T, 512 / E, true>(map, a, sms, st);
+    if (a.kmul != 1) {  // k-power tables (the ratio epilogue takes B-spline tables only)
+        switch (cw_bytes) {
+            case 128: return launch_t<KIND, T, 128 / E, false, true>(map, a, sms, st);
+            case 256: return launch_t<KIND, T, 256 / E, false, true>(map, a, sms, st);
+            default: return launch_t<KIND, T, 512 / E, false, true>(map, a, sms, st);
+        }
+    }
     switch (cw_bytes) {
         case 128: return launch_t<KIND, T, 128 / E, false>(map, a, sms, st);
         case 256: return launch_t<KIND, T, 256 / E, false>(map, a, sms, st);
@@ -540,10 +556,12 @@ int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const
         bucket_count_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, bucket, counts);
         if (dtype == SPO_F64)
             prologue_records_kernel<double>
-                <<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, bucket, counts, cursors, recs, status);
+                <<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, bucket, counts, cursors, recs, status,
+                                                   geo.kmul != 1);
         else
             prologue_records_kernel<float>
-                <<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, bucket, counts, cursors, recs, status);
+                <<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, bucket, counts, cursors, recs, status,
+                                                   geo.kmul != 1);
         int rc = check_launch("spo_eval (prologue) launch");
         if (rc) return rc;
     }
@@ -555,6 +573,9 @@ int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const
     a.bp = bp;
     a.nbatch = (n_pos + bp - 1) / bp;
     a.chunks = geo.nb / cw;
+    a.kmul = geo.kmul;
+    a.dz = g.dinv[2];
+    a.dz2 = 2.0 * g.dinv[2] * g.dinv[2];
     a.n_items = a.nbatch * (long long)geo.n_tiles * a.chunks;
     a.nb = geo.nb;
     a.out = out;

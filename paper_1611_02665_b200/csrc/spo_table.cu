@@ -7,6 +7,8 @@
 //                       SeedSequence(entropy=seed, spawn_key=(n,))), float32
 //                       draw = (u32 >> 8) * 2^-24, then *2 - 1 in fp32
 //   spo_fill_normal_f64 builder-defined Box-Muller N(0,1) on the same streams
+//   spo_pack_kpower     B-spline device layout -> k-power form (z-cubics in
+//                       the power basis; spo_b200.h SPO_TABLE_KPOWER)
 //
 // Every kernel walks the destination in its own layout (row-major over
 // (m, i', j', k', l)) so stores are fully coalesced; each element finds its
@@ -172,6 +174,35 @@ static int make_pack_geom(int dtype, int32_t n_splines, const int32_t *n3, int32
     return SPO_OK;
 }
 
+// k-power form: dst element (m, i', j', 4 k0 + r, l) from the four B-spline
+// rows k0..k0+3 of (m, i', j') in src.  Computed in fp64 (exact sums of fp32
+// inputs up to the divisions), rounded once.  With s(t) = sum_k a_k(t) c_k and
+// grid.py:127-130's a_k: 6 s = (c0 + 4c1 + c2) + 3t (c2 - c0)
+//   + 3t^2 (c0 - 2c1 + c2) + t^3 (-c0 + 3c1 - 3c2 + c3).
+template <typename T>
+__global__ void kpower_kernel(const T *__restrict__ src, long long total, int nb, int nz, T *__restrict__ dst) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int l = (int)(e % nb);
+        const long long row = e / nb;               // (m, i', j') * 4nz + 4 k0 + r
+        const int kr = (int)(row % (4LL * nz));
+        const long long ij = row / (4LL * nz);      // (m, i', j') flat
+        const int k0 = kr >> 2, r = kr & 3;
+        const T *c = src + (ij * (nz + 3) + k0) * (long long)nb + l;
+        const double c0 = (double)c[0], c1 = (double)c[nb], c2 = (double)c[2LL * nb], c3 = (double)c[3LL * nb];
+        double q;
+        // explicit round-to-nearest steps (no FMA contraction): the order of
+        // the expressions in spo_b200.h, reproducible on the host
+        switch (r) {
+            case 0: q = __ddiv_rn(__dadd_rn(__dadd_rn(c0, __dmul_rn(4.0, c1)), c2), 6.0); break;
+            case 1: q = __ddiv_rn(__dsub_rn(c2, c0), 2.0); break;
+            case 2: q = __ddiv_rn(__dadd_rn(__dsub_rn(c0, __dmul_rn(2.0, c1)), c2), 2.0); break;
+            default: q = __ddiv_rn(__dadd_rn(__dsub_rn(c3, c0), __dmul_rn(3.0, __dsub_rn(c1, c2))), 6.0); break;
+        }
+        dst[e] = (T)q;
+    }
+}
+
 static unsigned grid_for(long long total) {
     long long b = (total + 255) / 256;
     return (unsigned)(b < 148LL * 64 ? (b < 1 ? 1 : b) : 148LL * 64);
@@ -198,6 +229,26 @@ extern "C" int spo_pack_table(int dtype, const void *src, int32_t src_npad, int3
     else
         pack_kernel<float><<<grid_for(g.total), 256, 0, st>>>((const float *)src, src_npad, g, (float *)dst);
     return check_launch("spo_pack_table");
+}
+
+extern "C" int spo_pack_kpower(int dtype, const void *src, const int32_t *n3, int32_t nb, int32_t n_tiles,
+                               void *dst, void *stream) {
+    if (dtype != SPO_F32 && dtype != SPO_F64) return fail(SPO_ERR_CONTRACT, "unknown dtype %d", dtype);
+    TableGeom t;
+    int rc = make_geom(n3, nb, n_tiles, dtype, &t, true);
+    if (rc) return rc;
+    if (!src || !dst) return fail(SPO_ERR_CONTRACT, "NULL table pointer");
+    if (!aligned16(src) || !aligned16(dst)) return fail(SPO_ERR_CONTRACT, "tables must be 16-byte aligned");
+    rc = bind_device(dst);
+    if (rc) return rc;
+    if ((rc = check_on_device(src, "src table"))) return rc;
+    const long long total = t.tile_stride * n_tiles;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == SPO_F64)
+        kpower_kernel<double><<<grid_for(total), 256, 0, st>>>((const double *)src, total, nb, t.nz, (double *)dst);
+    else
+        kpower_kernel<float><<<grid_for(total), 256, 0, st>>>((const float *)src, total, nb, t.nz, (float *)dst);
+    return check_launch("spo_pack_kpower");
 }
 
 extern "C" int spo_fill_uniform(const uint64_t *keys, int32_t n_splines, const int32_t *n3,

@@ -261,6 +261,155 @@ __device__ __forceinline__ void slab_contract(const double *__restrict__ slab, c
     }
 }
 
+// ---- k-power form (SPO_FORM_KPOWER tables): the 4 rows of (i, j) hold the
+// power-basis coefficients q0..q3 of the cubic along k, so that
+//   sum_k a_k(t) c_k   = q0 + t q1 + t^2 q2 + t^3 q3            (= A)
+//   sum_k da_k/dt c_k  = q1 + 2t q2 + 3t^2 q3                   (= D)
+//   sum_k d2a_k/dt2 c_k / 2 = q2 + 3t q3                        (= H)
+// with a_k the uniform cubic B-spline basis of grid.py:127-130.  Seven packed
+// FMAs per (i, j) row group give all three k-sums (the B-spline form needs
+// twelve), and the only z weight is t itself.  The 1/dz and 2/dz^2 factors of
+// D and H are folded into the x weights of the streams that use them (axz =
+// ax/dz, daxz = dax/dz, axz2 = 2 ax/dz^2).
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
+template <int KIND>
+__device__ __forceinline__ void kpow_sums(float t, float2 q0, float2 q1, float2 q2, float2 q3, float2 &A, float2 &D,
+                                          float2 &H) {
+    const float2 e = fma2(t, q3, q2);  // q2 + t q3
+    A = fma2(t, fma2(t, e, q1), q0);
+    if (KIND != SPO_KIND_V) {
+        const float2 h = fma2(t, q3, e);  // q2 + 2t q3
+        D = fma2(t, add2(e, h), q1);      // q1 + t (2 q2 + 3t q3)
+        H = fma2(t, q3, h);               // q2 + 3t q3
+    }
+}
+template <int KIND>
+__device__ __forceinline__ void kpow_sums(double t, double q0, double q1, double q2, double q3, double &A, double &D,
+                                          double &H) {
+    const double e = __fma_rn(t, q3, q2);
+    A = __fma_rn(t, __fma_rn(t, e, q1), q0);
+    if (KIND != SPO_KIND_V) {
+        const double h = __fma_rn(t, q3, e);
+        D = __fma_rn(t, __dadd_rn(e, h), q1);
+        H = __fma_rn(t, q3, h);
+    }
+}
+
+// One i-slab of a k-power table for one lane (4 fp32 orbitals).
+template <int KIND, int CW>
+__device__ __forceinline__ void slab_contract_kp(const float *__restrict__ slab, const float (&wy)[12], float tz,
+                                                 float ax, float dax, float d2ax, float axz, float daxz, float axz2,
+                                                 float2 (&acc)[NS<KIND>::S][2]) {
+    float2 t00[2], t10[2], t01[2], t20[2], t11[2], t02[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) t00[h] = t10[h] = t01[h] = t20[h] = t11[h] = t02[h] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float4 c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const float4 *>(slab + (j * 4 + k) * CW);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float2 q0 = h ? make_float2(c[0].z, c[0].w) : make_float2(c[0].x, c[0].y);
+            const float2 q1 = h ? make_float2(c[1].z, c[1].w) : make_float2(c[1].x, c[1].y);
+            const float2 q2 = h ? make_float2(c[2].z, c[2].w) : make_float2(c[2].x, c[2].y);
+            const float2 q3 = h ? make_float2(c[3].z, c[3].w) : make_float2(c[3].x, c[3].y);
+            float2 A, D, H;
+            kpow_sums<KIND>(tz, q0, q1, q2, q3, A, D, H);
+            t00[h] = fma2(wy[j], A, t00[h]);
+            if (KIND != SPO_KIND_V) {
+                t10[h] = fma2(wy[4 + j], A, t10[h]);
+                t01[h] = fma2(wy[j], D, t01[h]);
+                t20[h] = fma2(wy[8 + j], A, t20[h]);
+                t02[h] = fma2(wy[j], H, t02[h]);
+                if (KIND == SPO_KIND_VGH) t11[h] = fma2(wy[4 + j], D, t11[h]);
+            }
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        acc[0][h] = fma2(ax, t00[h], acc[0][h]);
+        if (KIND != SPO_KIND_V) {
+            acc[1][h] = fma2(dax, t00[h], acc[1][h]);
+            acc[2][h] = fma2(ax, t10[h], acc[2][h]);
+            acc[3][h] = fma2(axz, t01[h], acc[3][h]);
+        }
+        if (KIND == SPO_KIND_VGL) acc[4][h] = fma2(d2ax, t00[h], fma2(ax, t20[h], fma2(axz2, t02[h], acc[4][h])));
+        if (KIND == SPO_KIND_VGH) {
+            acc[4][h] = fma2(d2ax, t00[h], acc[4][h]);
+            acc[5][h] = fma2(dax, t10[h], acc[5][h]);
+            acc[6][h] = fma2(daxz, t01[h], acc[6][h]);
+            acc[7][h] = fma2(ax, t20[h], acc[7][h]);
+            acc[8][h] = fma2(axz, t11[h], acc[8][h]);
+            acc[9][h] = fma2(axz2, t02[h], acc[9][h]);
+        }
+    }
+}
+
+// One i-slab of a k-power table for one lane (2 fp64 orbitals).
+template <int KIND, int CW>
+__device__ __forceinline__ void slab_contract_kp(const double *__restrict__ slab, const double (&wy)[12], double tz,
+                                                 double ax, double dax, double d2ax, double axz, double daxz,
+                                                 double axz2, double2 (&acc)[NS<KIND>::S][1]) {
+    double t00[2], t10[2], t01[2], t20[2], t11[2], t02[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) t00[e] = t10[e] = t01[e] = t20[e] = t11[e] = t02[e] = 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        double2 c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const double2 *>(slab + (j * 4 + k) * CW);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            double A, D, H;
+            kpow_sums<KIND>(tz, e ? c[0].y : c[0].x, e ? c[1].y : c[1].x, e ? c[2].y : c[2].x, e ? c[3].y : c[3].x,
+                            A, D, H);
+            t00[e] = __fma_rn(wy[j], A, t00[e]);
+            if (KIND != SPO_KIND_V) {
+                t10[e] = __fma_rn(wy[4 + j], A, t10[e]);
+                t01[e] = __fma_rn(wy[j], D, t01[e]);
+                t20[e] = __fma_rn(wy[8 + j], A, t20[e]);
+                t02[e] = __fma_rn(wy[j], H, t02[e]);
+                if (KIND == SPO_KIND_VGH) t11[e] = __fma_rn(wy[4 + j], D, t11[e]);
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        double *a0 = e ? &acc[0][0].y : &acc[0][0].x;
+        *a0 = __fma_rn(ax, t00[e], *a0);
+        if (KIND != SPO_KIND_V) {
+            double *a1 = e ? &acc[1][0].y : &acc[1][0].x;
+            double *a2 = e ? &acc[2][0].y : &acc[2][0].x;
+            double *a3 = e ? &acc[3][0].y : &acc[3][0].x;
+            *a1 = __fma_rn(dax, t00[e], *a1);
+            *a2 = __fma_rn(ax, t10[e], *a2);
+            *a3 = __fma_rn(axz, t01[e], *a3);
+        }
+        if (KIND == SPO_KIND_VGL) {
+            double *a4 = e ? &acc[4][0].y : &acc[4][0].x;
+            *a4 = __fma_rn(d2ax, t00[e], __fma_rn(ax, t20[e], __fma_rn(axz2, t02[e], *a4)));
+        }
+        if (KIND == SPO_KIND_VGH) {
+            double *a4 = e ? &acc[4][0].y : &acc[4][0].x;
+            double *a5 = e ? &acc[5][0].y : &acc[5][0].x;
+            double *a6 = e ? &acc[6][0].y : &acc[6][0].x;
+            double *a7 = e ? &acc[7][0].y : &acc[7][0].x;
+            double *a8 = e ? &acc[8][0].y : &acc[8][0].x;
+            double *a9 = e ? &acc[9][0].y : &acc[9][0].x;
+            *a4 = __fma_rn(d2ax, t00[e], *a4);
+            *a5 = __fma_rn(dax, t10[e], *a5);
+            *a6 = __fma_rn(daxz, t01[e], *a6);
+            *a7 = __fma_rn(ax, t20[e], *a7);
+            *a8 = __fma_rn(axz, t11[e], *a8);
+            *a9 = __fma_rn(axz2, t02[e], *a9);
+        }
+    }
+}
+
 template <typename T>
 struct Acc;
 template <>

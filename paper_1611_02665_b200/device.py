@@ -10,6 +10,13 @@ reproduces the reference's periodic indexing (kernels.py:153-157).
 Untiled tables are the M = 1 case (tile_size = N).  Tiled tables are the
 paper's AoSoA (coeffs.py:141-158, tile_table 197-210): M physically separate
 slices, so a tile-major sweep keeps one slice L2-resident.
+
+A table may also carry its k-power form (``with_kpower()``, spo_b200.h
+SPO_TABLE_KPOWER): ``kdata[m][i'][j'][4*k0 + r][l]`` holds the power-basis
+coefficients of the z-cubic of cell k0, which the FAST kernels contract with
+7 instead of 12 FMAs per row group (VGH: 248 instead of 328 per orbital).  It
+is derived from ``data`` on the device and used by FAST evaluations; STRICT
+mode and the fused ratio epilogue read ``data``.
 """
 from __future__ import annotations
 
@@ -103,6 +110,7 @@ class DeviceTable:
             raise ContractError(f"device data shape {tuple(data.shape)} != {shape}")
         self.data = data
         self.device = data.device
+        self.kdata = None  # k-power form (with_kpower)
 
     # ---------------------------------------------------------- geometry --
     @property
@@ -222,6 +230,34 @@ class DeviceTable:
         torch.cuda.current_stream(dt.device).synchronize()
         return dt
 
+    # ---------------------------------------------------- k-power form --
+    @property
+    def kpower_shape(self):
+        nx, ny, nz = self.grid.counts
+        return (self.n_tiles, nx + 3, ny + 3, 4 * nz, self.nb)
+
+    @property
+    def has_kpower(self) -> bool:
+        return self.kdata is not None
+
+    def with_kpower(self) -> "DeviceTable":
+        """Build (once) the k-power form of this table on its device and
+        return self.  Costs 4 nz / (nz + 3) times the table's memory (config
+        4: 18.8 GB next to the 4.9 GB B-spline form)."""
+        if self.kdata is None:
+            torch = _torch()
+            kd = torch.empty(self.kpower_shape, dtype=self.data.dtype, device=self.device)
+            _abi.check(_abi.load().spo_pack_kpower(self.dtype_code, self.data.data_ptr(),
+                                                   _abi.i32x3(self.grid.counts), self.nb, self.n_tiles,
+                                                   kd.data_ptr(), _stream_ptr(self.device)))
+            torch.cuda.current_stream(self.device).synchronize()
+            self.kdata = kd
+        return self
+
+    def drop_kpower(self) -> "DeviceTable":
+        self.kdata = None
+        return self
+
     def slice_orbitals(self, lo: int, hi: int, tile_size="auto") -> "DeviceTable":
         """A new device table holding splines [lo, hi) (orbital sharding)."""
         ref = self.reference_soa(device_result=True)
@@ -253,9 +289,10 @@ class DeviceTable:
         return out.cpu().numpy()
 
     def __repr__(self) -> str:
+        kp = f" + k-power form {self.kdata.numel() * self.kdata.element_size() / 1e9:.3f} GB" if self.has_kpower else ""
         return (f"DeviceTable(grid={self.grid.counts}, N={self.n_splines}, dtype={self.dtype.name}, "
                 f"tile_size={self.tile_size}, n_tiles={self.n_tiles}, nb={self.nb}, "
-                f"{self.nbytes / 1e9:.3f} GB on {self.device})")
+                f"{self.nbytes / 1e9:.3f} GB{kp} on {self.device})")
 
 
 _UPLOADS: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()

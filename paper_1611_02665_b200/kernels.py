@@ -199,8 +199,31 @@ def _positions_tensor(positions, device):
 PIPELINE_MIN_WORK = 1 << 19
 
 
+def _table_form(dt, kind, mode: str, form: str, P: int, ws_bytes: int):
+    """(data tensor, mode flag) of the table form a request runs on.  With
+    form="auto", FAST requests use the k-power form when the table carries one
+    and the request takes the line-window kernel (dense batches): there the
+    cheaper z-sums pay for the 4x larger table; sparse batches re-read more
+    table bytes per position and stay on the B-spline form
+    (scripts/bench_configs.py, profiles/r01/configs_kpower.md)."""
+    if form not in ("auto", "bspline", "kpower"):
+        raise ContractError(f"unknown table form {form!r}")
+    if form == "kpower" and mode != "fast":
+        raise ContractError("the k-power table form serves FAST evaluations only")
+    if form == "kpower" and not dt.has_kpower:
+        raise ContractError("the table has no k-power form (DeviceTable.with_kpower())")
+    if form == "kpower":
+        return dt.kdata, _abi.TABLE_KPOWER
+    if form == "auto" and mode == "fast" and dt.has_kpower:
+        code = _abi.load().spo_eval_path(kind.code, dt.dtype_code, _MODES[mode], _abi.i32x3(dt.grid.counts),
+                                         dt.nb, dt.n_tiles, P, max(ws_bytes, 0))
+        if _PATHS.get(code) == "line":
+            return dt.kdata, _abi.TABLE_KPOWER
+    return dt.data, 0
+
+
 def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=None,
-             status=None, check: bool = True, pipeline="auto", lane_limit=None):
+             status=None, check: bool = True, pipeline="auto", lane_limit=None, form: str = "auto"):
     """Evaluate `kind` at every position; returns out[P][S][lanes] (CUDA).
 
     table      DeviceTable (or any host table -> uploaded once and cached)
@@ -221,6 +244,10 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
                is then required and may live on another GPU (a peer
                device's memory or an IPC mapping of it): the fused
                evaluate + gather of multi.PeerGather
+    form       "auto" (FAST on the k-power form when the table carries one,
+               DeviceTable.with_kpower, and the batch is dense enough for the
+               line-window kernel), "bspline" or "kpower"; the two forms agree
+               within the FAST tolerance, not bitwise
     """
     torch = _torch()
     kind = as_kind(kind)
@@ -270,8 +297,9 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
     if pipeline == "auto":  # small batches: one generic launch beats prologue + TMA setup
         pipeline = P * dt.lanes >= PIPELINE_MIN_WORK
     ws_bytes = int(L.spo_eval_workspace_bytes(kind.code, dt.dtype_code, _MODES[mode], P)) if pipeline else 0
+    data, flag = _table_form(dt, kind, mode, form, P, ws_bytes)
     ws = torch.empty(max(ws_bytes, 0), dtype=torch.uint8, device=device) if ws_bytes > 0 else None
-    head = (kind.code, dt.dtype_code, _MODES[mode], dt.data.data_ptr(), _abi.i32x3(g.counts), dt.nb,
+    head = (kind.code, dt.dtype_code, _MODES[mode] | flag, data.data_ptr(), _abi.i32x3(g.counts), dt.nb,
             dt.n_tiles, _abi.f64x3(g.inverse_spacings), _abi.f64x3(g.spacings), pos.data_ptr(), P,
             out.data_ptr(), out.stride(0), out.stride(1))
     tail = (idx_ptr, status.data_ptr() if status is not None else None,
@@ -288,10 +316,11 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
 _PATHS = {0: "generic", 1: "tma", 2: "line"}
 
 
-def eval_path(table, kind, n_positions: int, *, mode: str = "fast", pipeline="auto") -> str:
+def eval_path(table, kind, n_positions: int, *, mode: str = "fast", pipeline="auto", form: str = "auto") -> str:
     """The kernel evaluate() runs for this request: "generic" (one pass),
     "tma" (per-position TMA pipeline) or "line" (planes shared along grid
-    lines) -- spo_eval_path; all give bitwise identical results."""
+    lines) -- spo_eval_path; all give bitwise identical results on the same
+    table form (eval_form() tells which form)."""
     kind = as_kind(kind)
     dt = as_device_table(table)
     L = _abi.load()
@@ -299,11 +328,24 @@ def eval_path(table, kind, n_positions: int, *, mode: str = "fast", pipeline="au
     if pipeline == "auto":
         pipeline = P * dt.lanes >= PIPELINE_MIN_WORK
     ws = int(L.spo_eval_workspace_bytes(kind.code, dt.dtype_code, _MODES[mode], P)) if pipeline else 0
-    code = L.spo_eval_path(kind.code, dt.dtype_code, _MODES[mode], _abi.i32x3(dt.grid.counts), dt.nb,
+    _, flag = _table_form(dt, kind, mode, form, P, ws)
+    code = L.spo_eval_path(kind.code, dt.dtype_code, _MODES[mode] | flag, _abi.i32x3(dt.grid.counts), dt.nb,
                            dt.n_tiles, P, max(ws, 0))
     if code < 0:
         raise ContractError("bad evaluation request")
     return _PATHS[code]
+
+
+def eval_form(table, kind, n_positions: int, *, mode: str = "fast", pipeline="auto", form: str = "auto") -> str:
+    """The table form evaluate() reads for this request: "bspline" or "kpower"."""
+    kind = as_kind(kind)
+    dt = as_device_table(table)
+    P = int(n_positions)
+    if pipeline == "auto":
+        pipeline = P * dt.lanes >= PIPELINE_MIN_WORK
+    ws = int(_abi.load().spo_eval_workspace_bytes(kind.code, dt.dtype_code, _MODES[mode], P)) if pipeline else 0
+    _, flag = _table_form(dt, kind, mode, form, P, ws)
+    return "kpower" if flag else "bspline"
 
 
 def evaluate_v(table, positions, out=None, **kw):

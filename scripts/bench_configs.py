@@ -62,6 +62,7 @@ def main():
     ap.add_argument("--configs", default="1,2,3,4,5")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--md", default=None)
+    ap.add_argument("--forms", default="bspline,kpower", help="table forms to time (spo_b200.h SPO_TABLE_KPOWER)")
     args = ap.parse_args()
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         peak = float(json.load(f)["hbm_gbs"])
@@ -81,7 +82,10 @@ def main():
             tables = {"full table": DeviceTable.random(cfg.grid, cfg.n_splines, seed=0)}
             pos = config_positions(cfg)
             item, q = 4, 32
-        for tname, dt in tables.items():
+        forms = args.forms.split(",")
+        for (tname, dt), form in [(t, f) for t in tables.items() for f in forms]:
+            if form == "kpower":
+                dt.with_kpower()
             for kind, p in pos.items():
                 if idx == 1:
                     p = p[:512]
@@ -93,12 +97,12 @@ def main():
 
                 def run():
                     for lo in range(0, P, c):
-                        evaluate(dt, kind, dp[lo: lo + c], out[: min(c, P - lo)], check=False)
+                        evaluate(dt, kind, dp[lo: lo + c], out[: min(c, P - lo)], check=False, form=form)
 
                 t = timed(run, args.reps)
                 bpp = bytes_per_position(kind, dt.n_splines, item, q)
                 gbs = bpp * P / t / 1e9
-                rows.append({"config": idx, "table": tname, "kind": kind, "positions": P,
+                rows.append({"config": idx, "table": tname, "form": form, "kind": kind, "positions": P,
                              "n_splines": dt.n_splines, "dtype": cfg.dtype, "seconds": t,
                              "orbital_evals_per_s": P * dt.n_splines / t, "algorithmic_gbs": gbs,
                              "fraction_of_hbm": gbs / peak})
@@ -107,11 +111,11 @@ def main():
         torch.cuda.empty_cache()
     if args.md:
         with open(args.md, "w") as f:
-            f.write("| cfg | table | kernel | positions | N | dtype | time (ms) | orbital-evals/s | "
+            f.write("| cfg | table | form | kernel | positions | N | dtype | time (ms) | orbital-evals/s | "
                     "algorithmic GB/s | fraction of %.1f GB/s |\n" % peak)
-            f.write("|---|---|---|---|---|---|---|---|---|---|\n")
+            f.write("|---|---|---|---|---|---|---|---|---|---|---|\n")
             for r in rows:
-                f.write(f"| {r['config']} | {r['table']} | {r['kind'].upper()} | {r['positions']:,} | "
+                f.write(f"| {r['config']} | {r['table']} | {r['form']} | {r['kind'].upper()} | {r['positions']:,} | "
                         f"{r['n_splines']} | {r['dtype']} | {r['seconds'] * 1e3:.3f} | "
                         f"{r['orbital_evals_per_s']:.3e} | {r['algorithmic_gbs']:,.0f} | "
                         f"{r['fraction_of_hbm']:.3f} |\n")

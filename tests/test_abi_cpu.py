@@ -34,7 +34,7 @@ def test_library_exports_every_header_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.spo_abi_version() == 5
+    assert lib.spo_abi_version() == 6
     assert lib.spo_eval_ratios_workspace_bytes(2, 0, 128, 32, 1000) > 1000 * 160 + 32 * 1000 * 10 * 8 - 1
     assert lib.spo_eval_ratios_workspace_bytes(2, 0, 96, 1, 1000) == -1  # 384-byte rows
     assert lib.spo_eval_workspace_bytes(2, 0, 0, 1000) >= 1000 * 160
@@ -65,6 +65,22 @@ def test_eval_argument_validation(lib):
     assert _eval(lib, n=0) == 0                                # empty batch: no-op
     assert _eval(lib, dinv=(0.0, 1.0, 1.0)) == 3
     assert b"positive" in lib.spo_last_error()
+    # k-power table form (SPO_TABLE_KPOWER): FAST only
+    assert _eval(lib, mode=1 | _abi.TABLE_KPOWER) == 3
+    assert b"B-spline table form" in lib.spo_last_error()
+    assert _eval(lib, mode=_abi.TABLE_KPOWER, n=0) == 0
+    assert _eval(lib, mode=0x200) == 1                          # unknown flag
+    assert lib.spo_eval_workspace_bytes(2, 0, _abi.TABLE_KPOWER, 1000) == lib.spo_eval_workspace_bytes(2, 0, 0, 1000)
+    assert lib.spo_eval_path(2, 0, 1 | _abi.TABLE_KPOWER, _abi.i32x3((16, 16, 16)), 64, 1, 10, 0) == -1
+
+
+def test_pack_kpower_validation(lib):
+    n3 = _abi.i32x3((8, 8, 8))
+    assert lib.spo_pack_kpower(5, 16, n3, 64, 1, 16, None) == 1     # dtype
+    assert lib.spo_pack_kpower(0, 16, n3, 48, 1, 16, None) == 1     # row not 128-byte
+    assert lib.spo_pack_kpower(0, None, n3, 64, 1, 16, None) == 1   # NULL
+    assert lib.spo_pack_kpower(0, 8, n3, 64, 1, 16, None) == 1      # misaligned
+    assert lib.spo_pack_kpower(0, 16, _abi.i32x3((8, 2, 8)), 64, 1, 16, None) == 3
 
 
 def _eval_lanes(lib, limit, **kw):
