@@ -31,6 +31,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "spo_common.cuh"
@@ -79,23 +80,34 @@ struct LT<double> {
     static constexpr int PREG = 40, CREG = 232;
     static constexpr int R = 22;      // plane slots (larger records)
 };
-template <typename T>
+// Warp split per table form.  The k-power form needs fewer registers (no z
+// weights), but 16 consumer warps at 112 registers spill and ran 10% slower
+// than 12 at 160 (31.8 vs 28.6 ms per 524,288-position launch), so both
+// forms use LT's split.
+template <typename T, bool KP>
+struct LW {
+    static constexpr int WGS = LT<T>::WGS, PREG = LT<T>::PREG, CREG = LT<T>::CREG;
+};
+template <typename T, bool KP = false>
 constexpr int cons_warps() {
-    return 4 * (LT<T>::WGS - 1);
+    return 4 * (LW<T, KP>::WGS - 1);
 }
-template <typename T>
+template <typename T, bool KP = false>
 constexpr int threads() {
-    return 128 * LT<T>::WGS;
+    return 128 * LW<T, KP>::WGS;
 }
 // The pool setmaxnreg redistributes is the CTA's launch allocation: threads x
 // the per-thread count __launch_bounds__ gives (64K / threads, rounded down to
 // a multiple of 8).  Growing past it would make TRY_ALLOC spin forever.
-template <typename T>
+template <typename T, bool KP = false>
 constexpr bool regs_fit() {
-    return 128 * LT<T>::PREG + 32 * cons_warps<T>() * LT<T>::CREG <= threads<T>() * (65536 / threads<T>() / 8 * 8);
+    return 128 * LW<T, KP>::PREG + 32 * cons_warps<T, KP>() * LW<T, KP>::CREG <=
+           threads<T, KP>() * (65536 / threads<T, KP>() / 8 * 8);
 }
 static_assert(regs_fit<float>(), "fp32 register split exceeds the launch allocation");
 static_assert(regs_fit<double>(), "fp64 register split exceeds the launch allocation");
+static_assert(regs_fit<float, true>(), "fp32 k-power register split exceeds the launch allocation");
+static_assert(regs_fit<double, true>(), "fp64 k-power register split exceeds the launch allocation");
 
 struct LArgs {
     const unsigned char *recs;  // [n_pos][RECB], sorted
@@ -128,7 +140,7 @@ struct LItem {
 
 // ------------------------------------------------------------- prologue --
 __global__ void line_keys_kernel(GridArgs g, const double *__restrict__ pos, long long n, unsigned *__restrict__ keys,
-                                 int *__restrict__ vals, int *__restrict__ status) {
+                                 int *__restrict__ vals, int *__restrict__ status, int3 nbk) {
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
          p += (long long)gridDim.x * blockDim.x) {
         double t;
@@ -138,7 +150,7 @@ __global__ void line_keys_kernel(GridArgs g, const double *__restrict__ pos, lon
         const int k0 = map_axis(z, g.dinv[2], g.cnt[2], &t);
         unsigned key = 0xffffffffu;
         if (isfinite(x) && isfinite(y) && isfinite(z)) {
-            const unsigned b = ((i0 * NBK / g.n[0]) * NBK + j0 * NBK / g.n[1]) * NBK + k0 * NBK / g.n[2];
+            const unsigned b = ((i0 * nbk.x / g.n[0]) * nbk.y + j0 * nbk.y / g.n[1]) * nbk.z + k0 * nbk.z / g.n[2];
             key = (b << 24) | ((unsigned)j0 << 16) | ((unsigned)k0 << 8) | (unsigned)i0;
         } else if (status) {
             atomicOr(status, 1);
@@ -236,9 +248,9 @@ static_assert(smem_bytes<double>() <= 232448, "shared memory budget");
 
 // ---------------------------------------------------------------- kernel --
 template <int KIND, typename T, bool RATIO, bool KP>
-__global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_constant__ CUtensorMap tmap, const LArgs a) {
+__global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_constant__ CUtensorMap tmap, const LArgs a) {
     constexpr int S = NS<KIND>::S;
-    constexpr int CONSUMERS = cons_warps<T>();
+    constexpr int CONSUMERS = cons_warps<T, KP>();
     constexpr int R = LT<T>::R;
     constexpr int W = 16 / (int)sizeof(T);         // lanes per thread (16-byte vector)
     constexpr int RECB = LT<T>::RECB;
@@ -274,7 +286,7 @@ __global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_cons
 
     if (warp < 4) {
         // ------------------------------------------------------ producer --
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(LT<T>::PREG));
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(LW<T, KP>::PREG));
         if (warp != 0) return;
         // lane 0 takes tickets and loads run records + plane lists; lanes
         // 0..PBATCH-1 issue the run's planes PBATCH at a time (one slot each)
@@ -379,7 +391,7 @@ __global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_cons
     // only on its own planes: `issued` says a plane's slot is armed (so the
     // parity wait is on the right phase), and relw[g] publishes the first
     // plane it will need next (all below are free for the producer).
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(LT<T>::CREG));
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(LW<T, KP>::CREG));
     const int g = warp - 4;
     unsigned base = 0;
     auto publish = [&](unsigned v) {
@@ -427,14 +439,8 @@ __global__ void __launch_bounds__(threads<T>(), 1) line_kernel(const __grid_cons
                 continue;
             }
             const unsigned s0 = base + (unsigned)(cell.z & 0xffff);
-            const T *w = reinterpret_cast<const T *>(rec);
             T wx[12], wy[12], wz[12];  // k-power tables: wz[0] = t_z, the rest unused
-#pragma unroll
-            for (int e = 0; e < 12; ++e) {
-                wx[e] = w[e];
-                wy[e] = w[12 + e];
-                wz[e] = w[24 + e];
-            }
+            load_weights(rec, wx, wy, wz);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const unsigned x = s0 + (unsigned)i;
@@ -480,7 +486,7 @@ static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t 
     int grid = (int)min((long long)sms, a.n_items);
     if (grid < 1) grid = 1;
     cudaFuncSetAttribute(line_kernel<KIND, T, RATIO, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    line_kernel<KIND, T, RATIO, KP><<<grid, threads<T>(), sm, st>>>(map, a);
+    line_kernel<KIND, T, RATIO, KP><<<grid, threads<T, KP>(), sm, st>>>(map, a);
     return check_launch("spo_eval (line) launch");
 }
 template <int KIND, typename T>
@@ -570,7 +576,14 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
 
     if (cudaMemsetAsync(ws, 0, WS_HEADER, st) != cudaSuccess) return check_launch("workspace reset");
     const long long blocks = min((n_pos + 255) / 256, 148LL * 16);
-    line_keys_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, keys_in, vals_in, status);
+    // spatial blocks per axis: k-power rows have no halo along z, so blocks
+    // flat in z cut the i/j halo re-reads (profiles/r01/nbk_sweep.txt)
+    int3 nbk = geo.kmul != 1 ? make_int3(2, 2, 4) : make_int3(NBK, NBK, NBK);
+    if (const char *e = getenv("SPO_NBK")) {  // experiment: blocks per axis "i,j,k"
+        sscanf(e, "%d,%d,%d", &nbk.x, &nbk.y, &nbk.z);
+        if (nbk.x * nbk.y * nbk.z > 255) nbk = make_int3(NBK, NBK, NBK);
+    }
+    line_keys_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, keys_in, vals_in, status, nbk);
     if (cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, vals, (int)n_pos, 0, 32, st) != cudaSuccess)
         return check_launch("spo_eval (line sort)");
     const int *order = vals.Current();  // the sorted original indices (either buffer)

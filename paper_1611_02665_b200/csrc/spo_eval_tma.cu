@@ -312,14 +312,8 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
         const unsigned char *rc = recs + cslot * BP * RECB;
         for (int g = 0; g < it.G; ++g) {
             const int p = g * PW + pp;
-            const T *w = reinterpret_cast<const T *>(rc + min(p, it.nb - 1) * RECB);
             T wx[12], wy[12], wz[12];
-#pragma unroll
-            for (int e = 0; e < 12; ++e) {
-                wx[e] = w[e];
-                wy[e] = w[12 + e];
-                wz[e] = w[24 + e];
-            }
+            load_weights(rc + min(p, it.nb - 1) * RECB, wx, wy, wz);
             const int4 cell = *reinterpret_cast<const int4 *>(rc + min(p, it.nb - 1) * RECB + 36 * sizeof(T));
             AV acc[S][AN];
 #pragma unroll

@@ -410,6 +410,27 @@ __device__ __forceinline__ void slab_contract_kp(const double *__restrict__ slab
     }
 }
 
+// The 36 weights of a record (16-byte aligned in shared memory) as 16-byte
+// loads: 9 (fp32) / 18 (fp64) LDS.128 instead of 36 scalar LDS -- uniform
+// addresses, one wavefront each.  Unused weights (k-power tables read only
+// wz[0]) are dropped by the compiler.
+template <typename T>
+__device__ __forceinline__ void load_weights(const unsigned char *rec, T (&wx)[12], T (&wy)[12], T (&wz)[12]) {
+    constexpr int E = 16 / (int)sizeof(T);
+    T w[36];
+#pragma unroll
+    for (int v = 0; v < 36 / E; ++v) {
+        const float4 q = reinterpret_cast<const float4 *>(rec)[v];
+        memcpy(&w[v * E], &q, 16);
+    }
+#pragma unroll
+    for (int e = 0; e < 12; ++e) {
+        wx[e] = w[e];
+        wy[e] = w[12 + e];
+        wz[e] = w[24 + e];
+    }
+}
+
 template <typename T>
 struct Acc;
 template <>
