@@ -20,7 +20,9 @@ There is no CPU path: everything below calls libspo_b200.so (spo_eval).
 from __future__ import annotations
 
 import ctypes
+import os
 import enum
+import threading
 
 import numpy as np
 
@@ -469,27 +471,77 @@ DROPIN_FREE_RESERVE = 16 << 30
 HOST_FINITE_CHECK_MAX = 4096
 
 
+# Host positions above this size are streamed through pinned staging buffers:
+# chunk k+1's host->device copy overlaps chunk k's evaluation.
+STAGED_MIN_BYTES = 1 << 20
+_staging = threading.local()
+
+
+def _staging_for(device, n_pos: int):
+    """Per thread and device: two pinned [n_pos][3] fp64 host buffers, two
+    device position buffers and a copy stream (grown on demand, reused)."""
+    torch = _torch()
+    cache = getattr(_staging, "by_device", None)
+    if cache is None:
+        cache = _staging.by_device = {}
+    key = (device.type, device.index)
+    st = cache.get(key)
+    if st is None or st["cap"] < n_pos:
+        st = {"cap": n_pos,
+              "host": [torch.empty((n_pos, 3), dtype=torch.float64).pin_memory() for _ in range(2)],
+              "dev": [torch.empty((n_pos, 3), dtype=torch.float64, device=device) for _ in range(2)],
+              "copy": torch.cuda.Stream(device),
+              "copied": [torch.cuda.Event() for _ in range(2)],
+              "used": [torch.cuda.Event() for _ in range(2)]}
+        cache[key] = st
+    return st
+
+
 def _eval_last(table, kind, pos: np.ndarray, mode: str):
     """Evaluate all positions on the device; return the last one's [S][lanes]
-    block on the host (reference batch semantics, kernels.py:353-354)."""
+    block on the host (reference batch semantics, kernels.py:353-354).
+    Large batches are streamed: chunk k+1's positions go host -> pinned ->
+    device on a copy stream while chunk k evaluates."""
     torch = _torch()
     dt = as_device_table(table)
     S = kind.output_streams_soa
     P = pos.shape[0]
     item = 8 if dt.dtype == np.float64 else 4
     per_pos = S * dt.lanes * item
-    free = torch.cuda.mem_get_info(dt.device)[0]
+    # free device memory, counting what torch's caching allocator holds
+    # unused (e.g. the previous call's scratch) as free
+    free = (torch.cuda.mem_get_info(dt.device)[0] + torch.cuda.memory_reserved(dt.device)
+            - torch.cuda.memory_allocated(dt.device))
     budget = min(DROPIN_SCRATCH_BYTES, max(free - DROPIN_FREE_RESERVE, per_pos))
     chunk = max(1, min(P, DROPIN_CHUNK, budget // per_pos))
+    if os.environ.get("SPO_DEBUG_DROPIN"):
+        print(f"[dropin] P={P} chunk={chunk} free={free / 2**30:.1f} GiB", flush=True)
     tdt = torch.float64 if dt.dtype == np.float64 else torch.float32
     scratch = torch.empty((chunk, S, dt.lanes), dtype=tdt, device=dt.device)
     status = torch.zeros(1, dtype=torch.int32, device=dt.device)
-    dpos = torch.from_numpy(pos).to(dt.device)
     last = None
-    for lo in range(0, P, chunk):
-        hi = min(P, lo + chunk)
-        evaluate(dt, kind, dpos[lo:hi], scratch, mode=mode, status=status, check=False)
-        last = hi - lo - 1
+    if pos.nbytes < STAGED_MIN_BYTES:
+        dpos = torch.from_numpy(pos).to(dt.device)
+        for lo in range(0, P, chunk):
+            hi = min(P, lo + chunk)
+            evaluate(dt, kind, dpos[lo:hi], scratch, mode=mode, status=status, check=False)
+            last = hi - lo - 1
+    else:
+        st = _staging_for(dt.device, chunk)
+        compute = torch.cuda.current_stream(dt.device)
+        for k, lo in enumerate(range(0, P, chunk)):
+            hi, b = min(P, lo + chunk), k & 1
+            st["copied"][b].synchronize()          # the pinned half is free again
+            host = st["host"][b][: hi - lo]
+            host.numpy()[:] = pos[lo:hi]
+            with torch.cuda.stream(st["copy"]):
+                st["copy"].wait_event(st["used"][b])  # evaluation of chunk k-2 read it
+                st["dev"][b][: hi - lo].copy_(host, non_blocking=True)
+                st["copied"][b].record(st["copy"])
+            compute.wait_event(st["copied"][b])
+            evaluate(dt, kind, st["dev"][b][: hi - lo], scratch, mode=mode, status=status, check=False)
+            st["used"][b].record(compute)
+            last = hi - lo - 1
     block = scratch[last].cpu().numpy()
     if int(status.item()) != 0:
         raise DomainError("positions contain non-finite components")
