@@ -449,7 +449,7 @@ def e2e_dropin(table, kind, pos_np, N, S, eval_batch, WalkerOutputsSoA, args, de
     import torch
 
     out = WalkerOutputsSoA(N)
-    steps = max(2, min(args.steps, 3))
+    steps = max(3, min(args.steps, 5))
     eval_batch(table, kind, pos_np, out, mode=args.mode)  # warm
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
