@@ -256,12 +256,22 @@ def run_b200(args):
     world, rank, local = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py --impl b200 needs a CUDA device")
+    n_dev = torch.cuda.device_count()
+    shared = world > n_dev  # more ranks than GPUs: a functional run only, never a measurement
+    if shared:
+        print(f"bench.py: {world} ranks on {n_dev} GPU(s): ranks share devices (gloo plumbing), "
+              "not a scaling measurement", file=sys.stderr, flush=True)
+        local %= n_dev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        # one rank per GPU over NCCL; NCCL refuses two ranks on one device
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     from paper_1611_02665_b200 import DeviceTable, KernelKind, WalkerOutputsSoA, eval_batch, evaluate
 
@@ -327,7 +337,7 @@ def run_b200(args):
     avg_launch_ms = sum(full) / len(full)
 
     # max over ranks
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cpu" if shared else dev)
     if world > 1:
         import torch.distributed as dist
 

@@ -41,3 +41,22 @@ def test_b200_arm_contract():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert d["config"]["path"] in ("line", "tma", "generic")
+
+
+@pytest.mark.gpu
+def test_b200_arm_two_ranks():
+    """The driver's N>1 launch (torchrun, one rank per GPU, NCCL): two ranks,
+    here sharing the test GPU when it has only one (a functional check of the
+    barrier / max-over-ranks / rank-0-prints path; bench.py warns that such a
+    run is not a measurement)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29613", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--config", "4", "--walkers", "64", "--chunk", "8192", "--steps", "2", "--warmup", "3", "--no-cpu",
+           "--no-e2e", "--form", "bspline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    assert d["config"]["parallelism"].startswith("walker-sharded x2")
