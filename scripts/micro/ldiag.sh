@@ -1,3 +1,5 @@
+# (the SPO_LDIAG / SPO_UGROUP hooks this drove were removed from spo_eval_line.cu after the
+# measurement; results in profiles/r01/line_energy_diag.txt)
 # line-kernel energy diagnostics (wrong results by design): SPO_LDIAG=1 drops the
 # output stores, =2 contracts only the first of each position's four planes
 for d in 0 1 2 3 0; do SPO_LDIAG=$d python bench.py --no-cpu --no-e2e --steps 10 > gpurun_out/ld.log 2>&1; python -c "
