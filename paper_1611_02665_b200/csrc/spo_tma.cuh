@@ -414,20 +414,26 @@ __device__ __forceinline__ void slab_contract_kp(const double *__restrict__ slab
 // loads: 9 (fp32) / 18 (fp64) LDS.128 instead of 36 scalar LDS -- uniform
 // addresses, one wavefront each.  Unused weights (k-power tables read only
 // wz[0]) are dropped by the compiler.
-template <typename T>
-__device__ __forceinline__ void load_weights(const unsigned char *rec, T (&wx)[12], T (&wy)[12], T (&wz)[12]) {
-    constexpr int E = 16 / (int)sizeof(T);
-    T w[36];
+__device__ __forceinline__ void load_weights(const unsigned char *rec, float (&wx)[12], float (&wy)[12],
+                                             float (&wz)[12]) {
+    const float4 *q = reinterpret_cast<const float4 *>(rec);
 #pragma unroll
-    for (int v = 0; v < 36 / E; ++v) {
-        const float4 q = reinterpret_cast<const float4 *>(rec)[v];
-        memcpy(&w[v * E], &q, 16);
+    for (int v = 0; v < 3; ++v) {
+        const float4 a = q[v], b = q[3 + v], c = q[6 + v];
+        wx[4 * v] = a.x, wx[4 * v + 1] = a.y, wx[4 * v + 2] = a.z, wx[4 * v + 3] = a.w;
+        wy[4 * v] = b.x, wy[4 * v + 1] = b.y, wy[4 * v + 2] = b.z, wy[4 * v + 3] = b.w;
+        wz[4 * v] = c.x, wz[4 * v + 1] = c.y, wz[4 * v + 2] = c.z, wz[4 * v + 3] = c.w;
     }
+}
+__device__ __forceinline__ void load_weights(const unsigned char *rec, double (&wx)[12], double (&wy)[12],
+                                             double (&wz)[12]) {
+    const double2 *q = reinterpret_cast<const double2 *>(rec);
 #pragma unroll
-    for (int e = 0; e < 12; ++e) {
-        wx[e] = w[e];
-        wy[e] = w[12 + e];
-        wz[e] = w[24 + e];
+    for (int v = 0; v < 6; ++v) {
+        const double2 a = q[v], b = q[6 + v], c = q[12 + v];
+        wx[2 * v] = a.x, wx[2 * v + 1] = a.y;
+        wy[2 * v] = b.x, wy[2 * v + 1] = b.y;
+        wz[2 * v] = c.x, wz[2 * v + 1] = c.y;
     }
 }
 
