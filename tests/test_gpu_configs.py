@@ -174,3 +174,64 @@ def test_config5_fp64_orbital_sharded(torch):
         ref, scale = oracle.eval_f64(kind, host, cfg.n_splines, cfg.grid.spacings, p[sel])
         ok, worst = oracle.tolerance_check(ref_full[sel].cpu().numpy(), ref, scale, TOL64)
         assert ok, (kind, worst)
+
+
+def test_config4_full_workload_kpower(torch):
+    """bench.py's exact regime: config 4 on the k-power table form in
+    524,288-position launches (line kernel): every output finite, sampled
+    positions of every launch within 1e-5 * sum|w*c| of the f64 oracle, and
+    the size-independent identities on the k-power form (V == VGH.v, VGL
+    gradients == VGH gradients, pipelined == generic, permutation
+    invariance) bitwise."""
+    from paper_1611_02665_b200.kernels import eval_form, eval_path
+
+    cfg = CONFIGS[4]
+    dt = DeviceTable.random(cfg.grid, cfg.n_splines, seed=0).with_kpower()
+    pos = config_positions(cfg)["vgh"]
+    chunk = 524288
+    assert eval_path(dt, "vgh", chunk) == "line" and eval_form(dt, "vgh", chunk) == "kpower"
+    out = torch.empty((chunk, 10, dt.lanes), dtype=torch.float32, device="cuda")
+    host = dt.reference_soa()
+    rng = np.random.default_rng(44)
+    for lo in range(0, len(pos), chunk):
+        evaluate(dt, "vgh", pos[lo: lo + chunk], out)
+        assert bool(torch.isfinite(out.sum()))  # any NaN/inf poisons the (fp32, no temporary) sum
+        sel = rng.choice(chunk, 12, replace=False)
+        ref, scale = oracle.eval_f64("vgh", host, 4096, cfg.grid.spacings, pos[lo + sel])
+        ok, worst = oracle.tolerance_check(out[sel].cpu().numpy(), ref, scale, TOL32)
+        assert ok, worst
+    del out, host
+    sub = pos[:65536]
+    base = evaluate(dt, "vgh", sub, form="kpower")
+    assert torch.equal(base, evaluate(dt, "vgh", sub, form="kpower", pipeline=False))
+    assert torch.equal(evaluate(dt, "v", sub, form="kpower")[:, 0], base[:, 0])
+    assert torch.equal(evaluate(dt, "vgl", sub, form="kpower")[:, 1:4], base[:, 1:4])
+    perm = np.random.default_rng(9).permutation(len(sub))
+    shuffled = torch.empty_like(base)
+    evaluate(dt, "vgh", sub[perm], shuffled, out_index=torch.from_numpy(perm).cuda(), form="kpower")
+    assert torch.equal(shuffled, base)
+
+
+def test_config5_fp64_orbital_sharded_kpower(torch):
+    """Config 5 on the k-power form: 8 orbital shards (each its own k-power
+    table) gathered == the full-N k-power evaluation bitwise, within 1e-12 *
+    sum|w*c| of the f64 oracle."""
+    cfg = CONFIGS[5]
+    full = DeviceTable.normal_f64(cfg.grid, cfg.n_splines, seed=0).with_kpower()
+    pos = config_positions(cfg, walkers=range(32))
+    part = OrbitalPartition.make(cfg.n_splines, 8, quantum=16)
+    host = full.reference_soa()
+    for kind in ("v", "vgl", "vgh"):
+        p = pos[kind]
+        ref_full = evaluate(full, kind, p, form="kpower")[:, :, : cfg.n_splines]
+        gathered = torch.empty_like(ref_full)
+        for r in range(8):
+            lo, hi = part.local(r)
+            shard = full.slice_orbitals(lo, hi).with_kpower()
+            gathered[:, :, lo:hi] = evaluate(shard, kind, p, form="kpower")[:, :, : hi - lo]
+            del shard
+        assert torch.equal(gathered, ref_full)
+        sel = np.random.default_rng(6).choice(len(p), 8, replace=False)
+        ref, scale = oracle.eval_f64(kind, host, cfg.n_splines, cfg.grid.spacings, p[sel])
+        ok, worst = oracle.tolerance_check(ref_full[sel].cpu().numpy(), ref, scale, TOL64)
+        assert ok, (kind, worst)
