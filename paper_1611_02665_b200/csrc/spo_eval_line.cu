@@ -33,6 +33,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "spo_common.cuh"
 #include "spo_prologue.cuh"
@@ -247,7 +248,7 @@ static_assert(smem_bytes<float>() <= 232448, "shared memory budget");
 static_assert(smem_bytes<double>() <= 232448, "shared memory budget");
 
 // ---------------------------------------------------------------- kernel --
-template <int KIND, typename T, bool RATIO, bool KP>
+template <int KIND, typename T, bool RATIO, bool KP, int VGROUP = 1>
 __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_constant__ CUtensorMap tmap, const LArgs a) {
     constexpr int S = NS<KIND>::S;
     constexpr int CONSUMERS = cons_warps<T, KP>();
@@ -398,6 +399,100 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
         __syncwarp();
         if (lane == 0) st_release_shared(&relw[g], v);
     };
+    if constexpr (KIND == SPO_KIND_V && !RATIO && VGROUP > 1) {
+        // V: groups of VGROUP consecutive sorted positions, group k of a run
+        // to warp k mod CONSUMERS.  V has little math per plane, so a plane's
+        // shared-memory read is most of its cost: the group reads each plane
+        // of [lo, hi] (the union of its positions' planes, contiguous in load
+        // order) once, and every position covering it consumes the registers
+        // (v_rowgroup, bitwise the one-position sequence).  Ring safety as
+        // below: the warp publishes lo, and hi <= lo + 4 VGROUP - 1 < lo + R.
+        constexpr int VM = VGROUP;
+        static_assert(4 * VM <= R, "a group's planes must fit the ring");
+        using RV = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+        using TV = typename std::conditional<sizeof(T) == 4, float2, double>::type;
+        for (int r = 0;; ++r) {
+            const int slot = r & 1;
+            mbar_wait(&rfull[slot], (r >> 1) & 1);
+            const LItem it = info[slot];
+            if (!it.valid) break;
+            const unsigned char *rc = recs + slot * BPL * RECB;
+            const unsigned count = (unsigned)reinterpret_cast<const int4 *>(rc + 36 * sizeof(T))->z >> 16;
+            auto first_plane = [&](int q) -> unsigned {  // base + count once q is past the run
+                if (q >= it.nb) return base + count;
+                const int4 c = *reinterpret_cast<const int4 *>(rc + q * RECB + 36 * sizeof(T));
+                return c.x < 0 ? base + count : base + (unsigned)(c.z & 0xffff);
+            };
+            publish(first_plane(g * VM));
+            const long long L0 = (long long)it.u * ULANES + lane * W;
+            const int nv = (int)max(0LL, min((long long)W, a.lane_limit - L0));
+            for (int q0 = g * VM; q0 < it.nb; q0 += CONSUMERS * VM) {
+                T wx[VM][4], wy[VM][4], wz[VM][4];
+                unsigned s0[VM];
+                bool live[VM];
+                long long op[VM];
+                AV acc[VM][1][AN];
+                TV t00[VM][2];
+                unsigned lo = 0xffffffffu, hi = 0;
+#pragma unroll
+                for (int m = 0; m < VM; ++m) {
+                    const bool in = q0 + m < it.nb;
+                    const unsigned char *rec = rc + min(q0 + m, it.nb - 1) * RECB;
+                    const int4 cell = *reinterpret_cast<const int4 *>(rec + 36 * sizeof(T));
+                    live[m] = in && cell.x >= 0;
+                    op[m] = !in ? -1 : (a.out_index ? a.out_index[cell.w] : cell.w);
+                    // the a-rows of x, y, z: weights 0..3, 12..15, 24..27 (k-power: wz[0] = t_z)
+                    load4(rec, wx[m]);
+                    load4(rec + 12 * sizeof(T), wy[m]);
+                    load4(rec + 24 * sizeof(T), wz[m]);
+                    s0[m] = base + (unsigned)(cell.z & 0xffff);
+                    if (live[m]) {
+                        lo = min(lo, s0[m]);
+                        hi = max(hi, s0[m] + 3u);
+                    }
+#pragma unroll
+                    for (int h = 0; h < AN; ++h) zero(acc[m][0][h]);
+                    t00[m][0] = t00[m][1] = TV{};
+                }
+                for (unsigned x = lo; lo != 0xffffffffu && x <= hi; ++x) {
+                    while (ld_acquire_shared(issued) <= x) __nanosleep(SPIN_NS);
+                    const int sl = (int)(x % R);
+                    mbar_wait(&full[sl], (x / R) & 1);
+                    const T *p = reinterpret_cast<const T *>(planes + (size_t)sl * PLANE) + lane * W;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        RV c[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const RV *>(p + (j * 4 + k) * BOXL);
+#pragma unroll
+                        for (int m = 0; m < VM; ++m)
+                            if (live[m] && x - s0[m] < 4u) v_rowgroup<KP>(c, wz[m], wy[m][j], t00[m]);
+                    }
+#pragma unroll
+                    for (int m = 0; m < VM; ++m)
+                        if (live[m] && x - s0[m] < 4u) {
+                            const unsigned i = x - s0[m];
+                            const T ax = i == 0 ? wx[m][0] : (i == 1 ? wx[m][1] : (i == 2 ? wx[m][2] : wx[m][3]));
+                            v_plane_done(ax, t00[m], acc[m]);
+                        }
+                }
+                publish(first_plane(q0 + CONSUMERS * VM));  // this group's planes are read
+#pragma unroll
+                for (int m = 0; m < VM; ++m) {
+                    if (op[m] < 0) continue;
+                    T *o = reinterpret_cast<T *>(a.out) + op[m] * a.out_pos_stride + L0;
+                    if (nv == W)
+                        store_lane<1>(o, a.out_stream_stride, acc[m], live[m]);
+                    else if (nv > 0)
+                        store_lane_partial<1>(o, a.out_stream_stride, acc[m], live[m], nv);
+                }
+            }
+            base += count;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&rempty[slot]);
+        }
+        return;
+    }
     for (int r = 0;; ++r) {
         const int slot = r & 1;
         mbar_wait(&rfull[slot], (r >> 1) & 1);
@@ -480,14 +575,27 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
     }
 }
 
-template <int KIND, typename T, bool RATIO, bool KP>
-static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
+template <int KIND, typename T, bool RATIO, bool KP, int VGROUP = 1>
+static int launch1(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
     constexpr size_t sm = smem_bytes<T>();
     int grid = (int)min((long long)sms, a.n_items);
     if (grid < 1) grid = 1;
-    cudaFuncSetAttribute(line_kernel<KIND, T, RATIO, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    line_kernel<KIND, T, RATIO, KP><<<grid, threads<T, KP>(), sm, st>>>(map, a);
+    cudaFuncSetAttribute(line_kernel<KIND, T, RATIO, KP, VGROUP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    line_kernel<KIND, T, RATIO, KP, VGROUP><<<grid, threads<T, KP>(), sm, st>>>(map, a);
     return check_launch("spo_eval (line) launch");
+}
+template <int KIND, typename T, bool RATIO, bool KP>
+static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
+    if constexpr (KIND == SPO_KIND_V && !RATIO) {
+        // V positions per consumer warp: 2 (fp32) / 4 (fp64), measured by
+        // scripts/micro/vm_sweep.py (profiles/r01/v_groups.jsonl); SPO_VGROUP=1/2/4 forces
+        const char *e = getenv("SPO_VGROUP");
+        const int v = e ? atoi(e) : (sizeof(T) == 4 ? 2 : 4);
+        if (v == 2) return launch1<KIND, T, RATIO, KP, 2>(map, a, sms, st);
+        if (v == 4) return launch1<KIND, T, RATIO, KP, 4>(map, a, sms, st);
+    }
+    return launch1<KIND, T, RATIO, KP>(map, a, sms, st);
 }
 template <int KIND, typename T>
 static int launch_r(bool ratio, bool kp, const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {

@@ -410,6 +410,63 @@ __device__ __forceinline__ void slab_contract_kp(const double *__restrict__ slab
     }
 }
 
+// ---- V, several positions per consumer warp (the line kernel's VGROUP
+// path): one row group (the 4 k-rows of one j) of a plane contracted for one
+// position into its per-plane j-sum t00 -- exactly the V sequence of
+// slab_contract / slab_contract_kp (bitwise), so a plane's rows are read from
+// shared memory once for every position of the group that covers the plane.
+template <bool KP>
+__device__ __forceinline__ void v_rowgroup(const float4 (&c)[4], const float (&wz)[4], float wyj, float2 (&t00)[2]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const float2 c0 = h ? make_float2(c[0].z, c[0].w) : make_float2(c[0].x, c[0].y);
+        const float2 c1 = h ? make_float2(c[1].z, c[1].w) : make_float2(c[1].x, c[1].y);
+        const float2 c2 = h ? make_float2(c[2].z, c[2].w) : make_float2(c[2].x, c[2].y);
+        const float2 c3 = h ? make_float2(c[3].z, c[3].w) : make_float2(c[3].x, c[3].y);
+        float2 s0, d, hh;
+        if constexpr (KP)
+            kpow_sums<SPO_KIND_V>(wz[0], c0, c1, c2, c3, s0, d, hh);
+        else
+            s0 = fma2(wz[3], c3, fma2(wz[2], c2, fma2(wz[1], c1, mul2(wz[0], c0))));
+        t00[h] = fma2(wyj, s0, t00[h]);
+    }
+}
+template <bool KP>
+__device__ __forceinline__ void v_rowgroup(const double2 (&c)[4], const double (&wz)[4], double wyj,
+                                           double (&t00)[2]) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const double c0 = e ? c[0].y : c[0].x, c1 = e ? c[1].y : c[1].x;
+        const double c2 = e ? c[2].y : c[2].x, c3 = e ? c[3].y : c[3].x;
+        double s0, d, hh;
+        if constexpr (KP)
+            kpow_sums<SPO_KIND_V>(wz[0], c0, c1, c2, c3, s0, d, hh);
+        else
+            s0 = __fma_rn(wz[3], c3, __fma_rn(wz[2], c2, __fma_rn(wz[1], c1, wz[0] * c0)));
+        t00[e] = __fma_rn(wyj, s0, t00[e]);
+    }
+}
+__device__ __forceinline__ void v_plane_done(float ax, float2 (&t00)[2], float2 (&acc)[1][2]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        acc[0][h] = fma2(ax, t00[h], acc[0][h]);
+        t00[h] = make_float2(0.f, 0.f);
+    }
+}
+__device__ __forceinline__ void v_plane_done(double ax, double (&t00)[2], double2 (&acc)[1][1]) {
+    acc[0][0].x = __fma_rn(ax, t00[0], acc[0][0].x);
+    acc[0][0].y = __fma_rn(ax, t00[1], acc[0][0].y);
+    t00[0] = t00[1] = 0.0;
+}
+__device__ __forceinline__ void load4(const unsigned char *p, float (&w)[4]) {
+    const float4 v = *reinterpret_cast<const float4 *>(p);
+    w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+}
+__device__ __forceinline__ void load4(const unsigned char *p, double (&w)[4]) {
+    const double2 v0 = reinterpret_cast<const double2 *>(p)[0], v1 = reinterpret_cast<const double2 *>(p)[1];
+    w[0] = v0.x, w[1] = v0.y, w[2] = v1.x, w[3] = v1.y;
+}
+
 // The 36 weights of a record (16-byte aligned in shared memory) as 16-byte
 // loads: 9 (fp32) / 18 (fp64) LDS.128 instead of 36 scalar LDS -- uniform
 // addresses, one wavefront each.  Unused weights (k-power tables read only

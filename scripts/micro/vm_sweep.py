@@ -1,7 +1,7 @@
 #!/usr/bin/env python
-"""V on the line kernel: one position per consumer warp (SPO_VM=0) vs groups of
-consecutive positions per warp (default), and the per-position TMA kernel, in
-the sustained regime, per density / dtype / table form.
+"""V on the line kernel: SPO_VGROUP = 1, 2 or 4 consecutive positions per
+consumer warp, and the per-position TMA kernel, in the sustained regime (all
+variants in one process, interleaved), per density / dtype / table form.
     python scripts/micro/vm_sweep.py [grid] [N] [densities] [f32|f64] [bspline|kpower]"""
 import json
 import os
@@ -54,9 +54,9 @@ def main():
         pos = torch.from_numpy(np.random.default_rng(P).random((P, 3))).cuda()
         out = torch.empty((P, 1, dt.lanes), device="cuda", dtype=torch.float64 if f64 else torch.float32)
         res = {}
-        for name, line, vm in (("tma", "0", "1"), ("line1", "1", "0"), ("lineVM", "1", "1"),
-                               ("line1", "1", "0"), ("lineVM", "1", "1")):
-            os.environ["SPO_LINE"], os.environ["SPO_VM"] = line, vm
+        for name, line, vm in (("tma", "0", "1"), ("line1", "1", "1"), ("line2", "1", "2"), ("line4", "1", "4"),
+                               ("line1", "1", "1"), ("line2", "1", "2"), ("line4", "1", "4")):
+            os.environ["SPO_LINE"], os.environ["SPO_VGROUP"] = line, vm
             res.setdefault(name, []).append(round(rate(lambda: evaluate(dt, "v", pos, out, check=False,
                                                                         form=form, pipeline=True)), 3))
         print(json.dumps({"grid": n_grid, "N": n, "dtype": "f64" if f64 else "f32", "form": form, "density": d,
