@@ -588,10 +588,12 @@ static int launch1(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t
 template <int KIND, typename T, bool RATIO, bool KP>
 static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
     if constexpr (KIND == SPO_KIND_V && !RATIO) {
-        // V positions per consumer warp: 2 (fp32) / 4 (fp64), measured by
+        // V positions per consumer warp: 2 (fp32), 4 (fp64 k-power), 1 (fp64
+        // B-spline: its 4 z weights per position cost more registers than the
+        // shared reads save below ~16 positions per cell), measured by
         // scripts/micro/vm_sweep.py (profiles/r01/v_groups.jsonl); SPO_VGROUP=1/2/4 forces
         const char *e = getenv("SPO_VGROUP");
-        const int v = e ? atoi(e) : (sizeof(T) == 4 ? 2 : 4);
+        const int v = e ? atoi(e) : (sizeof(T) == 4 ? 2 : (KP ? 4 : 1));
         if (v == 2) return launch1<KIND, T, RATIO, KP, 2>(map, a, sms, st);
         if (v == 4) return launch1<KIND, T, RATIO, KP, 4>(map, a, sms, st);
     }

@@ -67,7 +67,7 @@ def main():
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         peak = float(json.load(f)["hbm_gbs"])
     rows = []
-    chunk = 1 << 18  # positions per launch, as bench.py
+    chunk = 1 << 18  # launch-size quantum
     for idx in [int(c) for c in args.configs.split(",")]:
         cfg = CONFIGS[idx]
         if cfg.dtype == "f64":
@@ -92,7 +92,11 @@ def main():
                 P = p.shape[0]
                 dp = torch.from_numpy(np.ascontiguousarray(p)).cuda()
                 S = {"v": 1, "vgl": 5, "vgh": 10}[kind]
-                c = min(chunk, P)
+                # positions per launch: as many as ~40 GB of outputs allow (the
+                # batched driver's regime; config 4 VGH: 2^18, as bench.py on a
+                # box without room for 2^19)
+                item_b = 8 if cfg.dtype == "f64" else 4
+                c = min(P, max(chunk, (40 << 30) // (S * dt.lanes * item_b) // chunk * chunk))
                 out = torch.empty((c, S, dt.lanes), dtype=dt.data.dtype, device="cuda")
 
                 def run():
