@@ -387,11 +387,15 @@ def run_b200(args):
         "clocks": clocks.summary(wall0, wall1),
     }
 
-    if rank == 0 and not args.no_e2e:
+    if not args.no_e2e:
         del out  # the drop-in path sizes its own scratch from the free memory
         torch.cuda.empty_cache()
-        result["e2e"] = e2e_dropin(table, kind, pos_np, N, S, eval_batch, WalkerOutputsSoA, args, dev)
-        result["e2e_full_outputs"] = e2e_full_outputs(table, kind, pos_np, N, S, dev)
+        # every rank drives its own GPU through the drop-in API at once; the
+        # job's e2e time is the slowest rank's
+        e2e = e2e_dropin(table, kind, pos_np, N, S, eval_batch, WalkerOutputsSoA, args, dev, world, shared)
+        if rank == 0:
+            result["e2e"] = e2e
+            result["e2e_full_outputs"] = e2e_full_outputs(table, kind, pos_np, N, S, dev)
     if world > 1:
         import torch.distributed as dist
 
@@ -450,25 +454,35 @@ def e2e_full_outputs(table, kind, pos_np, N, S, dev, chunk=8192, seconds=2.0):
             "sample": f"{k} chunks of {chunk} positions, all outputs to pinned host memory"}
 
 
-def e2e_dropin(table, kind, pos_np, N, S, eval_batch, WalkerOutputsSoA, args, dev):
+def e2e_dropin(table, kind, pos_np, N, S, eval_batch, WalkerOutputsSoA, args, dev, world=1, shared=False):
     """Same metric through the reference-facing drop-in call eval_batch with
     HOST buffers: host positions -> device each step, all positions evaluated,
     the last position's streams copied back into the host WalkerOutputsSoA
     (the reference API's output, kernels.py:353-354).  Timed by wall clock
-    around fully synchronous calls (the call returns host data)."""
+    around fully synchronous calls (the call returns host data); under
+    torchrun every rank runs at once and the job time is the max over ranks
+    (whole-job value = all ranks' positions / that time)."""
     import torch
 
     out = WalkerOutputsSoA(N)
     steps = max(3, min(args.steps, 5))
     eval_batch(table, kind, pos_np, out, mode=args.mode)  # warm
     torch.cuda.synchronize(dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         eval_batch(table, kind, pos_np, out, mode=args.mode)
     dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt], dtype=torch.float64, device="cpu" if shared else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
     P = pos_np.shape[0]
-    return {"value": P * N * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(pos_np.nbytes),
-            "d2h_bytes_per_step": int(S * table.lanes * 4),
+    return {"value": world * P * N * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(world * pos_np.nbytes),
+            "d2h_bytes_per_step": int(world * S * table.lanes * 4), "ranks": world,
             "api": "paper_1611_02665_b200.eval_batch(table, kind, host positions, host WalkerOutputsSoA)"}
 
 

@@ -52,7 +52,7 @@ def test_b200_arm_two_ranks():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", "29613", os.path.join(ROOT, "bench.py"), "--gpus", "2",
            "--config", "4", "--walkers", "64", "--chunk", "8192", "--steps", "2", "--warmup", "3", "--no-cpu",
-           "--no-e2e", "--form", "bspline"]
+           "--form", "bspline"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -60,3 +60,5 @@ def test_b200_arm_two_ranks():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
     assert d["config"]["parallelism"].startswith("walker-sharded x2")
+    e = d["e2e"]  # whole-job: both ranks' positions over the slower rank's time
+    assert e["ranks"] == 2 and e["value"] > 0 and e["h2d_bytes_per_step"] == 2 * 64 * 256 * 24
