@@ -132,6 +132,7 @@ struct LArgs {
     // power-basis rows per cell), z-derivative factors 1/dz and 2/dz^2
     int kmul;
     double dz, dz2;
+    int rotate;                 // rotate the run's positions over the consumer warps
 };
 
 struct LItem {
@@ -423,10 +424,16 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                 const int4 c = *reinterpret_cast<const int4 *>(rc + q * RECB + 36 * sizeof(T));
                 return c.x < 0 ? base + count : base + (unsigned)(c.z & 0xffff);
             };
-            publish(first_plane(g * VM));
+            // group k of the run goes to warp (k + rotation) mod CONSUMERS; the
+            // rotation advances by the run's group count so that every warp gets
+            // the same share of groups over consecutive runs (64 / VM groups do
+            // not divide evenly among the warps)
+            const int rot = a.rotate ? (int)((long long)r * (BPL / VM) % CONSUMERS) : 0;
+            const int k0 = (g + CONSUMERS - rot) % CONSUMERS;
+            publish(first_plane(k0 * VM));
             const long long L0 = (long long)it.u * ULANES + lane * W;
             const int nv = (int)max(0LL, min((long long)W, a.lane_limit - L0));
-            for (int q0 = g * VM; q0 < it.nb; q0 += CONSUMERS * VM) {
+            for (int q0 = k0 * VM; q0 < it.nb; q0 += CONSUMERS * VM) {
                 T wx[VM][4], wy[VM][4], wz[VM][4];
                 unsigned s0[VM];
                 bool live[VM];
@@ -505,10 +512,16 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
             const int4 c = *reinterpret_cast<const int4 *>(rc + q * RECB + 36 * sizeof(T));
             return c.x < 0 ? base + count : base + (unsigned)(c.z & 0xffff);
         };
-        publish(first_plane(g));
+        // position q of the run goes to warp (q + rotation) mod CONSUMERS; the
+        // rotation advances by BPL per run, so the warps take turns at the
+        // BPL mod CONSUMERS extra positions (64 = 5 x 12 + 4: without it four
+        // warps would always carry a sixth position and the rest would wait)
+        const int rot = a.rotate ? (int)((long long)r * BPL % CONSUMERS) : 0;
+        const int q_first = (g + CONSUMERS - rot) % CONSUMERS;
+        publish(first_plane(q_first));
         const long long L0 = (long long)it.u * ULANES + lane * W;  // output lane
         const int nv = (int)max(0LL, min((long long)W, a.lane_limit - L0));
-        for (int q = g; q < it.nb; q += CONSUMERS) {
+        for (int q = q_first; q < it.nb; q += CONSUMERS) {
             const unsigned char *rec = rc + q * RECB;
             const int4 cell = *reinterpret_cast<const int4 *>(rec + 36 * sizeof(T));
             const long long op = a.out_index ? a.out_index[cell.w] : cell.w;
@@ -730,6 +743,8 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     a.partials = ratio ? reinterpret_cast<double *>(ws + eval_line_workspace_bytes(dtype, n_pos)) : nullptr;
     const bool kp = geo.kmul != 1;
     a.kmul = geo.kmul;
+    const char *env_rot = getenv("SPO_ROTATE");  // experiment: 0 = fixed position-to-warp assignment
+    a.rotate = !(env_rot && env_rot[0] == '0');
     a.dz = g.dinv[2];
     a.dz2 = 2.0 * g.dinv[2] * g.dinv[2];
 
