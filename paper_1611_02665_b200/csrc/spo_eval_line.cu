@@ -133,6 +133,7 @@ struct LArgs {
     int kmul;
     double dz, dz2;
     int rotate;                 // rotate the run's positions over the consumer warps
+    int dynamic;                // consumers take positions from a shared per-run counter
 };
 
 struct LItem {
@@ -272,10 +273,11 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
     unsigned *issued = relw + CONSUMERS;                      // planes armed so far
     unsigned long long *rfull = full + 2 * R;
     unsigned long long *rempty = rfull + 2;
-    static_assert((CONSUMERS + 1) * 4 <= R * 8, "release words fit");
+    unsigned *qnext = issued + 1;                             // [2]: next position of each record slot's run
+    static_assert((CONSUMERS + 3) * 4 <= R * 8, "release words fit");
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x < CONSUMERS + 1) relw[threadIdx.x] = 0;  // and issued
+    if (threadIdx.x < CONSUMERS + 3) relw[threadIdx.x] = 0;  // and issued, qnext
     if (threadIdx.x == 0) {
         for (int s = 0; s < R; ++s) mbar_init(&full[s], 1);
         for (int s = 0; s < 2; ++s) {
@@ -305,6 +307,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                 it.b0 = b * BPL;
                 it.nb = (int)min((long long)BPL, a.n_pos - it.b0);
                 info[slot] = it;
+                qnext[slot] = 0;  // published to the consumers by the arrive (release)
                 mbar_arrive_expect_tx(&rfull[slot], (unsigned)(it.nb * RECB + PLB));
                 bulk_load(recs + slot * BPL * RECB, a.recs + it.b0 * RECB, (unsigned)(it.nb * RECB), &rfull[slot]);
                 bulk_load(plists + slot * PL, a.plist + b * PL, (unsigned)PLB, &rfull[slot]);
@@ -517,11 +520,19 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
         // BPL mod CONSUMERS extra positions (64 = 5 x 12 + 4: without it four
         // warps would always carry a sixth position and the rest would wait)
         const int rot = a.rotate ? (int)((long long)r * BPL % CONSUMERS) : 0;
-        const int q_first = (g + CONSUMERS - rot) % CONSUMERS;
+        // dynamic: every warp takes the run's next position from a shared
+        // counter, so the warps stay on neighbouring positions (one window of
+        // planes) whatever their individual delays
+        auto take = [&]() -> int {
+            int v = 0;
+            if (lane == 0) v = (int)atomicAdd(&qnext[slot], 1u);
+            return __shfl_sync(0xffffffffu, v, 0);
+        };
+        const int q_first = a.dynamic ? take() : (g + CONSUMERS - rot) % CONSUMERS;
         publish(first_plane(q_first));
         const long long L0 = (long long)it.u * ULANES + lane * W;  // output lane
         const int nv = (int)max(0LL, min((long long)W, a.lane_limit - L0));
-        for (int q = q_first; q < it.nb; q += CONSUMERS) {
+        for (int q = q_first, qn = 0; q < it.nb; q = qn) {
             const unsigned char *rec = rc + q * RECB;
             const int4 cell = *reinterpret_cast<const int4 *>(rec + 36 * sizeof(T));
             const long long op = a.out_index ? a.out_index[cell.w] : cell.w;
@@ -532,7 +543,8 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
 #pragma unroll
                 for (int h = 0; h < AN; ++h) zero(acc[s][h]);
             if (cell.x < 0) {
-                publish(first_plane(q + CONSUMERS));
+                qn = a.dynamic ? take() : q + CONSUMERS;
+                publish(first_plane(qn));
                 if constexpr (RATIO) {
                     if (lane == 0) {
                         double *dst = a.partials + ((long long)it.u * a.n_pos + cell.w) * S;
@@ -564,7 +576,8 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                     slab_contract<KIND, BOXL>(p, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
                 }
             }
-            publish(first_plane(q + CONSUMERS));  // this position's planes are read
+            qn = a.dynamic ? take() : q + CONSUMERS;
+            publish(first_plane(qn));  // this position's planes are read
             if constexpr (RATIO) {
                 // the warp's 32 lanes are this position's unit: dot with the
                 // coefficient row, reduced over the warp (as spo_eval_tma.cu)
@@ -745,6 +758,10 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     a.kmul = geo.kmul;
     const char *env_rot = getenv("SPO_ROTATE");  // experiment: 0 = fixed position-to-warp assignment
     a.rotate = !(env_rot && env_rot[0] == '0');
+    // positions from a shared per-run counter (default; SPO_DYNAMIC=0: the
+    // rotated static assignment).  +0.3-1% (scripts/micro/dynamic_ab.sh)
+    const char *env_dyn = getenv("SPO_DYNAMIC");
+    a.dynamic = !(env_dyn && env_dyn[0] == '0');
     a.dz = g.dinv[2];
     a.dz2 = 2.0 * g.dinv[2] * g.dinv[2];
 
