@@ -134,6 +134,7 @@ static void eval_one_f32(int kind, const float *data, int nx, int ny, int nz, in
                 const float *restrict row = data + ((ii * ny + jj) * nz + kk) * (int64_t)npad;
                 float pv = ax[i] * ay[j] * az[k];
                 if (kind == ORC_V) {
+#pragma omp simd
                     for (int n = 0; n < npad; ++n) v[n] += pv * row[n];
                     continue;
                 }
@@ -144,6 +145,9 @@ static void eval_one_f32(int kind, const float *data, int nx, int ny, int nz, in
                     float pl = d2ax[i] * ay[j] * az[k] + ax[i] * d2ay[j] * az[k] +
                                ax[i] * ay[j] * d2az[k];
                     float *restrict l = out + 4 * sstride;
+                    /* the streams and the row never alias: let GCC vectorise
+                       (too many pointer pairs for its runtime alias checks) */
+#pragma omp simd
                     for (int n = 0; n < npad; ++n) {
                         float c = row[n];
                         v[n] += pv * c;
@@ -163,6 +167,7 @@ static void eval_one_f32(int kind, const float *data, int nx, int ny, int nz, in
                 float *restrict hxx = out + 4 * sstride, *restrict hxy = out + 5 * sstride,
                                 *restrict hxz = out + 6 * sstride, *restrict hyy = out + 7 * sstride,
                                 *restrict hyz = out + 8 * sstride, *restrict hzz = out + 9 * sstride;
+#pragma omp simd
                 for (int n = 0; n < npad; ++n) {
                     float c = row[n];
                     v[n] += pv * c;
