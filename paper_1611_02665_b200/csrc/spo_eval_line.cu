@@ -134,6 +134,7 @@ struct LArgs {
     double dz, dz2;
     int rotate;                 // rotate the run's positions over the consumer warps
     int dynamic;                // consumers take positions from a shared per-run counter
+    long long cells;            // grid cells (positions per cell pick the V group size)
 };
 
 struct LItem {
@@ -614,14 +615,18 @@ static int launch1(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t
 template <int KIND, typename T, bool RATIO, bool KP>
 static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
     if constexpr (KIND == SPO_KIND_V && !RATIO) {
-        // V positions per consumer warp: 2 (fp32), 4 (fp64 k-power), 1 (fp64
-        // B-spline: its 4 z weights per position cost more registers than the
-        // shared reads save below ~16 positions per cell), measured by
-        // scripts/micro/vm_sweep.py (profiles/r01/v_groups.jsonl); SPO_VGROUP=1/2/4 forces
+        // V positions per consumer warp by density (scripts/micro/vm_sweep.py,
+        // profiles/r01/v_groups.jsonl): fp32 2 below 3.5 positions per cell,
+        // else 4; fp64 k-power 4; fp64 B-spline 1 below 4 per cell (its 4 z
+        // weights per position cost registers), else 4.  SPO_VGROUP=1..5 forces.
         const char *e = getenv("SPO_VGROUP");
-        const int v = e ? atoi(e) : (sizeof(T) == 4 ? 2 : (KP ? 4 : 1));
+        const double dens = (double)a.n_pos / (double)a.cells;
+        const int v = e ? atoi(e)
+                        : (sizeof(T) == 4 ? (dens < 3.5 ? 2 : 4) : (KP ? 4 : (dens < 4.0 ? 1 : 4)));
         if (v == 2) return launch1<KIND, T, RATIO, KP, 2>(map, a, sms, st);
         if (v == 4) return launch1<KIND, T, RATIO, KP, 4>(map, a, sms, st);
+        if (v == 3) return launch1<KIND, T, RATIO, KP, 3>(map, a, sms, st);
+        if (v == 5) return launch1<KIND, T, RATIO, KP, 5>(map, a, sms, st);
     }
     return launch1<KIND, T, RATIO, KP>(map, a, sms, st);
 }
@@ -756,6 +761,7 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     a.partials = ratio ? reinterpret_cast<double *>(ws + eval_line_workspace_bytes(dtype, n_pos)) : nullptr;
     const bool kp = geo.kmul != 1;
     a.kmul = geo.kmul;
+    a.cells = (long long)geo.nx * geo.ny * geo.nz;
     const char *env_rot = getenv("SPO_ROTATE");  // experiment: 0 = fixed position-to-warp assignment
     a.rotate = !(env_rot && env_rot[0] == '0');
     // positions from a shared per-run counter (default; SPO_DYNAMIC=0: the

@@ -54,8 +54,8 @@ def main():
         pos = torch.from_numpy(np.random.default_rng(P).random((P, 3))).cuda()
         out = torch.empty((P, 1, dt.lanes), device="cuda", dtype=torch.float64 if f64 else torch.float32)
         res = {}
-        for name, line, vm in (("tma", "0", "1"), ("line1", "1", "1"), ("line2", "1", "2"), ("line4", "1", "4"),
-                               ("line1", "1", "1"), ("line2", "1", "2"), ("line4", "1", "4")):
+        groups = os.environ.get("VM_SWEEP", "1,2,4").split(",")
+        for name, line, vm in [("tma", "0", "1")] + [(f"line{v}", "1", v) for v in groups] * 2:
             os.environ["SPO_LINE"], os.environ["SPO_VGROUP"] = line, vm
             res.setdefault(name, []).append(round(rate(lambda: evaluate(dt, "v", pos, out, check=False,
                                                                         form=form, pipeline=True)), 3))
