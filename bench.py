@@ -367,6 +367,11 @@ def run_b200(args):
                 "peak_source": peak_src, "kernel": kernel_name,
                 "algorithmic_bytes_per_position": bpp, "positions_per_launch": chunk,
                 "avg_launch_ms": avg_launch_ms}
+    if roofline["traffic"]:
+        # what DRAM actually carried (ncu bytes of the same launch shape over this
+        # run's launch time): frac > 1 above means the table came from L2
+        roofline["dram_gbs"] = roofline["traffic"] / (avg_launch_ms * 1e-3) / 1e9
+        roofline["dram_frac"] = roofline["dram_gbs"] / peak
 
     result = {
         "metric": METRIC if kind == "vgh" else f"B-spline {kind.upper()} orbital-evals/s",
