@@ -48,11 +48,15 @@ def retile(table: DeviceTable, tile_size) -> DeviceTable:
 
 
 def tune_tile_size(table: DeviceTable, kind, n_positions: int = 1 << 16, repeats: int = 3,
-                   seed: int = 1, candidates=None) -> TuneResult:
-    """Scan tilings of `table` for `kind`; returns the argmax (ties -> larger tile)."""
+                   seed: int = 1, candidates=None, kpower=None) -> TuneResult:
+    """Scan tilings of `table` for `kind`; returns the argmax (ties -> larger tile).
+    kpower: give every candidate the k-power table form (None: as `table`), so
+    FAST requests are timed on the form evaluate() would pick."""
     import torch
 
     kind = as_kind(kind)
+    if kpower is None:
+        kpower = table.has_kpower
     cands = list(candidates) if candidates is not None else tile_candidates(table.n_splines)
     moves = 256
     walkers = max(1, -(-n_positions // moves))
@@ -63,6 +67,8 @@ def tune_tile_size(table: DeviceTable, kind, n_positions: int = 1 << 16, repeats
     stream = torch.cuda.current_stream(table.device)
     for nb in cands:
         t = retile(table, None if nb >= table.n_splines else nb)
+        if kpower:
+            t.with_kpower()
         out = torch.empty((pos.shape[0], kind.output_streams_soa, t.lanes), dtype=t.data.dtype,
                           device=t.device)
         evaluate(t, kind, pos, out, check=False)  # warm-up
