@@ -44,50 +44,61 @@ def load(build_if_missing: bool = True):
             return _lib
         from .build import needs_build
 
+        alt = os.environ.get("SPO_LIB")  # experiments: a variant build of the library
+        if alt:
+            L = ctypes.CDLL(alt)
+            _bind(L)
+            _lib = L
+            return L
         if needs_build():
             if not build_if_missing:
                 raise RuntimeError(f"{LIB_PATH} is missing or stale; run paper_1611_02665_b200.build")
             from .build import build
             build()
         L = ctypes.CDLL(LIB_PATH)
-        i32, i64, dbl, vp, ip = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_int
-        P = ctypes.POINTER
-        L.spo_abi_version.restype = ip
-        L.spo_last_error.restype = ctypes.c_char_p
-        L.spo_eval.restype = ip
-        L.spo_eval.argtypes = [ip, ip, ip, vp, P(i32), i32, i32, P(dbl), P(dbl), vp, i64, vp, i64,
-                               i64, vp, vp, vp, i64, vp]
-        L.spo_eval_lanes.restype = ip
-        L.spo_eval_lanes.argtypes = [ip, ip, ip, vp, P(i32), i32, i32, P(dbl), P(dbl), vp, i64, vp, i64,
-                                     i64, i64, vp, vp, vp, i64, vp]
-        L.spo_eval_path.restype = ip
-        L.spo_eval_path.argtypes = [ip, ip, ip, P(i32), i32, i32, i64, i64]
-        L.spo_eval_workspace_bytes.restype = i64
-        L.spo_eval_workspace_bytes.argtypes = [ip, ip, ip, i64]
-        L.spo_eval_ratios_workspace_bytes.restype = i64
-        L.spo_eval_ratios_workspace_bytes.argtypes = [ip, ip, i32, i32, i64]
-        L.spo_eval_ratios.restype = ip
-        L.spo_eval_ratios.argtypes = [ip, ip, vp, P(i32), i32, i32, P(dbl), P(dbl), vp, i64, vp, i64, vp, vp,
-                                      vp, i64, vp]
-        L.spo_prologue.restype = ip
-        L.spo_prologue.argtypes = [ip, P(i32), P(dbl), P(dbl), vp, i64, vp, vp, vp, vp]
-        L.spo_basis_weights.restype = ip
-        L.spo_basis_weights.argtypes = [ip, vp, i64, dbl, dbl, vp, vp]
-        L.spo_pack_table.restype = ip
-        L.spo_pack_table.argtypes = [ip, vp, i32, i32, P(i32), i32, i32, i32, vp, vp]
-        L.spo_pack_kpower.restype = ip
-        L.spo_pack_kpower.argtypes = [ip, vp, P(i32), i32, i32, vp, vp]
-        L.spo_fill_uniform.restype = ip
-        L.spo_fill_uniform.argtypes = [vp, i32, P(i32), i32, i32, i32, vp, vp]
-        L.spo_fill_normal_f64.restype = ip
-        L.spo_fill_normal_f64.argtypes = [vp, i32, P(i32), i32, i32, i32, vp, vp]
-        u64 = ctypes.c_uint64
-        L.spo_fill_positions.restype = ip
-        L.spo_fill_positions.argtypes = [u64, i64, i64, u64, u64, i64, P(dbl), vp, vp]
-        if L.spo_abi_version() != ABI_VERSION:
-            raise RuntimeError("libspo_b200.so ABI version mismatch; rebuild")
+        _bind(L)
         _lib = L
         return L
+
+
+def _bind(L):
+    """Declare the ctypes signatures of include/spo_b200.h and check the ABI version."""
+    i32, i64, dbl, vp, ip = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_int
+    P = ctypes.POINTER
+    L.spo_abi_version.restype = ip
+    L.spo_last_error.restype = ctypes.c_char_p
+    L.spo_eval.restype = ip
+    L.spo_eval.argtypes = [ip, ip, ip, vp, P(i32), i32, i32, P(dbl), P(dbl), vp, i64, vp, i64,
+                           i64, vp, vp, vp, i64, vp]
+    L.spo_eval_lanes.restype = ip
+    L.spo_eval_lanes.argtypes = [ip, ip, ip, vp, P(i32), i32, i32, P(dbl), P(dbl), vp, i64, vp, i64,
+                                 i64, i64, vp, vp, vp, i64, vp]
+    L.spo_eval_path.restype = ip
+    L.spo_eval_path.argtypes = [ip, ip, ip, P(i32), i32, i32, i64, i64]
+    L.spo_eval_workspace_bytes.restype = i64
+    L.spo_eval_workspace_bytes.argtypes = [ip, ip, ip, i64]
+    L.spo_eval_ratios_workspace_bytes.restype = i64
+    L.spo_eval_ratios_workspace_bytes.argtypes = [ip, ip, i32, i32, i64]
+    L.spo_eval_ratios.restype = ip
+    L.spo_eval_ratios.argtypes = [ip, ip, vp, P(i32), i32, i32, P(dbl), P(dbl), vp, i64, vp, i64, vp, vp,
+                                  vp, i64, vp]
+    L.spo_prologue.restype = ip
+    L.spo_prologue.argtypes = [ip, P(i32), P(dbl), P(dbl), vp, i64, vp, vp, vp, vp]
+    L.spo_basis_weights.restype = ip
+    L.spo_basis_weights.argtypes = [ip, vp, i64, dbl, dbl, vp, vp]
+    L.spo_pack_table.restype = ip
+    L.spo_pack_table.argtypes = [ip, vp, i32, i32, P(i32), i32, i32, i32, vp, vp]
+    L.spo_pack_kpower.restype = ip
+    L.spo_pack_kpower.argtypes = [ip, vp, P(i32), i32, i32, vp, vp]
+    L.spo_fill_uniform.restype = ip
+    L.spo_fill_uniform.argtypes = [vp, i32, P(i32), i32, i32, i32, vp, vp]
+    L.spo_fill_normal_f64.restype = ip
+    L.spo_fill_normal_f64.argtypes = [vp, i32, P(i32), i32, i32, i32, vp, vp]
+    u64 = ctypes.c_uint64
+    L.spo_fill_positions.restype = ip
+    L.spo_fill_positions.argtypes = [u64, i64, i64, u64, u64, i64, P(dbl), vp, vp]
+    if L.spo_abi_version() != ABI_VERSION:
+        raise RuntimeError("libspo_b200.so ABI version mismatch; rebuild")
 
 
 def check(rc: int) -> None:

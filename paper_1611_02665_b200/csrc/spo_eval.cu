@@ -158,7 +158,6 @@ __device__ __forceinline__ void contract_fast(const T *__restrict__ rp, long lon
                 }
             }
         }
-#pragma unroll
         // z-derivative x weights: the B-spline form carries 1/dz in wz; the
         // k-power form folds it here (axz = ax/dz, daxz = dax/dz, axz2 = 2ax/dz^2)
         const T axz = KP ? mulT(wx[i], dz) : wx[i], daxz = KP ? mulT(wx[4 + i], dz) : wx[4 + i];

@@ -49,7 +49,16 @@ constexpr int BOXB = 512;                        // TMA box width in bytes
 static_assert(ROWB == BOXB, "one TMA box per plane");
 constexpr int BOX = 16 * BOXB;                   // bytes per box (16 rows)
 constexpr int PLANE = 16 * ROWB;                 // bytes per plane slot
-constexpr int BPL = 64;                          // positions per item
+#ifndef SPO_LINE_BPL
+#define SPO_LINE_BPL 64
+#endif
+#ifndef SPO_LINE_R32
+#define SPO_LINE_R32 24
+#endif
+#ifndef SPO_LINE_R64
+#define SPO_LINE_R64 22
+#endif
+constexpr int BPL = SPO_LINE_BPL;                // positions per item (run)
 constexpr int PL = 4 * BPL + 4;                  // plane-list ints per run: count, planes, pad
 constexpr int PLB = PL * 4;                      // plane-list bytes per run (16-byte multiple)
 constexpr unsigned SPIN_NS = 256;                // back-off of the issued / release polls
@@ -72,14 +81,14 @@ struct LT<float> {
     static constexpr int RECB = 36 * 4 + 16;
     static constexpr int WGS = 4;     // 12 consumer warps, 3 per SMSP
     static constexpr int PREG = 32, CREG = 160;
-    static constexpr int R = 24;      // plane slots
+    static constexpr int R = SPO_LINE_R32;  // plane slots
 };
 template <>
 struct LT<double> {
     static constexpr int RECB = 36 * 8 + 16;
     static constexpr int WGS = 3;     // 8 consumer warps: fp64 weights need ~200 registers
     static constexpr int PREG = 40, CREG = 232;
-    static constexpr int R = 22;      // plane slots (larger records)
+    static constexpr int R = SPO_LINE_R64;  // plane slots (larger records)
 };
 // Warp split per table form.  The k-power form needs fewer registers (no z
 // weights), but 16 consumer warps at 112 registers spill and ran 10% slower
@@ -626,7 +635,8 @@ static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t 
         if (v == 2) return launch1<KIND, T, RATIO, KP, 2>(map, a, sms, st);
         if (v == 4) return launch1<KIND, T, RATIO, KP, 4>(map, a, sms, st);
         if (v == 3) return launch1<KIND, T, RATIO, KP, 3>(map, a, sms, st);
-        if (v == 5) return launch1<KIND, T, RATIO, KP, 5>(map, a, sms, st);
+        if constexpr (4 * 5 <= LT<T>::R)
+            if (v == 5) return launch1<KIND, T, RATIO, KP, 5>(map, a, sms, st);
     }
     return launch1<KIND, T, RATIO, KP>(map, a, sms, st);
 }
