@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--kind", default="vgh")
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--kpower", action="store_true", help="give the tables the k-power form (dense batches use it)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -58,12 +59,19 @@ def main():
         full = DeviceTable.normal_f64(grid, args.splines, seed=7, device=dev)
     lo, hi = part.local(rank)
     mine = full.slice_orbitals(lo, hi)
+    if args.kpower:
+        full.with_kpower()
+        mine.with_kpower()
     rng = np.random.default_rng(11)
     pos = torch.from_numpy(rng.random((args.positions, 3)) * 2.0 - 0.5).to(dev)
 
     pg = PeerGather(part, args.kind, args.positions, full.dtype, root=0, device=dev)
     got = pg.evaluate(mine, pos)
     res = {"world": world, "backend": backend, "ranks_share_gpu": not own_gpu, "bounds": part.bounds}
+    if args.kpower:
+        from paper_1611_02665_b200.kernels import eval_form
+
+        res["form"] = eval_form(mine, args.kind, args.positions)
     if rank == 0:
         want = evaluate(full, args.kind, pos)[:, :, : args.splines]
         res["peer_bitwise"] = bool(torch.equal(got, want))

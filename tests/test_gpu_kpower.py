@@ -202,3 +202,40 @@ def test_kpower_auto_policy():
     assert eval_form(dt, "vgh", len(dense), mode="strict") == "bspline"
     assert torch.equal(evaluate(dt, "vgh", dense), evaluate(dt, "vgh", dense, form="kpower"))
     assert torch.equal(evaluate(dt, "vgh", sparse), evaluate(dt, "vgh", sparse, form="bspline"))
+
+
+def test_kpower_from_host_aos_and_soa():
+    """Reference host tables (SoA and AoS layouts, build_table) uploaded, given
+    the k-power form: both layouts evaluate bitwise alike on it, within the
+    tolerance of the oracle."""
+    import torch
+
+    from paper_1611_02665_b200 import FillSpec, build_table
+    from paper_1611_02665_b200.grid import GridSpec
+
+    grid = GridSpec(14, 14, 14, 1.0 / 14, 1.0 / 14, 1.0 / 14)
+    soa = DeviceTable.from_host(build_table(grid, 96, FillSpec.random(5))).with_kpower()
+    aos = DeviceTable.from_host(build_table(grid, 96, FillSpec.random(5), layout="aos")).with_kpower()
+    pos = np.random.default_rng(3).random((3 * 14 ** 3, 3))
+    a = evaluate(soa, "vgh", pos, form="kpower")
+    b = evaluate(aos, "vgh", pos, form="kpower")
+    assert torch.equal(a, b)
+    ok, worst = _oracle_ok(soa, "vgh", a, pos, 1e-5, np.arange(0, len(pos), 41))
+    assert ok, worst
+
+
+def test_kpower_graph_replay():
+    """A CUDA graph of a dense k-power evaluation replays bitwise."""
+    import torch
+
+    from paper_1611_02665_b200.graphs import GraphedEvaluator
+    from paper_1611_02665_b200.kernels import eval_form
+
+    dt = DeviceTable.random(unit_cell_grid(16), 256, seed=2).with_kpower()
+    P = 2 * 16 ** 3
+    assert eval_form(dt, "vgh", P) == "kpower"
+    ge = GraphedEvaluator(dt, "vgh", P)
+    for seed in (1, 2):
+        pos = np.random.default_rng(seed).random((P, 3))
+        got = ge.run(torch.from_numpy(pos).cuda()).clone()
+        assert torch.equal(got, evaluate(dt, "vgh", pos))

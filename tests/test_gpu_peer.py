@@ -65,3 +65,16 @@ def test_peer_gather_two_ranks(dtype, n):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     res = json.loads([line for line in r.stdout.splitlines() if line.startswith("{")][-1])
     assert res["peer_bitwise"] and res["world"] == 2
+
+
+def test_peer_gather_two_ranks_kpower():
+    """The fused gather on the k-power form: a dense batch (line kernel) on each
+    rank's k-power slice, gathered == the full-N k-power evaluation bitwise."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.join(ROOT, "scripts", "peer_gather_check.py"), "--splines", "256", "--positions", "40000",
+           "--kpower", "--reps", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    res = json.loads([line for line in r.stdout.splitlines() if line.startswith("{")][-1])
+    assert res["peer_bitwise"] and res["world"] == 2 and res["form"] == "kpower"
