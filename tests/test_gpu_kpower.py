@@ -239,3 +239,18 @@ def test_kpower_graph_replay():
         pos = np.random.default_rng(seed).random((P, 3))
         got = ge.run(torch.from_numpy(pos).cuda()).clone()
         assert torch.equal(got, evaluate(dt, "vgh", pos))
+
+
+def test_kpower_through_eval_batch():
+    """The drop-in eval_batch (host positions, reference last-sample output)
+    on a table that carries the k-power form: dense batches run on it."""
+    from paper_1611_02665_b200 import WalkerOutputsSoA, collect_streams, eval_batch
+
+    dt = DeviceTable.random(unit_cell_grid(16), 128, seed=6).with_kpower()
+    pos = np.random.default_rng(9).random((3 * 16 ** 3 + 5, 3))
+    out = WalkerOutputsSoA(128)
+    eval_batch(dt, "vgh", pos, out)
+    want = streams(evaluate(dt, "vgh", pos[-1:], form="kpower"), dt, "vgh")
+    got = collect_streams(out, KernelKind("vgh"))
+    for name in KernelKind("vgh").stream_names:
+        assert np.array_equal(got[name], want[name].cpu().numpy()[0]), name
