@@ -2,33 +2,52 @@
 """Benchmark: B-spline VGH orbital-evals/s on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config 4] [--chunk 0] [--mode fast] [--tile 0]
+                    [--config 4] [--scaling strong|weak] [--chunk 0] [--mode fast]
+                    [--tile -1] [--form bspline|kpower]
 
 Workload (default, BASELINE config 4 -- the VGH config with N >= 2048 the
 north-star roofline target names): 64^3 periodic grid (67^3 wrap-padded),
 N = 4096 fp32 orbitals, FillSpec.random(0) table (generated on the device,
 bit-identical to the reference's numpy fill), 4096 walkers x 256 moves =
-1,048,576 VGH positions per GPU per step (Philox walker streams, seed 1).
-A step evaluates all of them, in launches of `--chunk` positions into a
-reusable output buffer (every output is written to HBM; the reference also
-overwrites its output buffer per position, kernels.py:353-354).  --chunk 0
-(default): 524,288 positions per launch (2 per grid cell: more stencil planes
-shared by the line kernel) when the GPU has room for the 86 GB output buffer,
-else 262,144.
+1,048,576 VGH positions per step (Philox walker streams, seed 1).  A step
+evaluates all of them, in launches of `--chunk` positions into a reusable
+output buffer (every output is written to HBM; the reference also overwrites
+its output buffer per position, kernels.py:353-354).  --chunk 0 (default):
+524,288 positions per launch (2 per grid cell: more stencil planes shared by
+the line kernel) when the GPU has room for the 86 GB output buffer, else
+262,144.  `value` is timed on the default B-spline table form (the north-star
+error bound for every input); the opt-in k-power form is timed beside it as
+the extra key "kpower" (its error bound is weaker).
 
-Multi-GPU (torchrun, one rank per GPU): walker-sharded, table replicated,
-each rank evaluates its own 4096-walker population (weak scaling), no
-collective on the data path; time = max over ranks.
+Multi-GPU (torchrun, one rank per GPU): walker-sharded, table replicated, no
+collective on the data path; time = max over ranks.  --scaling strong
+(default): the config's 4096 walkers are split over the N ranks
+(multi.walker_shard), as BASELINE.md quotes config 4 (194.8 ms on 1 GPU,
+24.4 ms on 8); a weak-scaling figure (every rank a full population) is added
+as the key "weak".  --scaling weak swaps the two.
 
-Printed JSON (rank 0): value = orbital-evals/s over all ranks; roofline of
-the eval kernel (algorithmic bytes 64*Npad*4 + 10*Npad*4 per position over
-the measured HBM copy bandwidth); e2e through the drop-in API eval_batch with
-host buffers; cpu_baseline = the C restatement of the reference fp32 kernels
-(oracle/, kind "port") on the host cores.
+--config 5: fp64, N = 4096 orbital-sharded over the ranks (N/world splines
+each, generated directly on the rank), 16384 walkers x 128 positions with the
+12:1:1 V:VGL:VGH mix (position index mod 14); every rank evaluates every
+position on its slice and the full-N outputs are gathered on rank 0.  `value`
+times the fused evaluate + gather (multi.PeerGather: the kernel's own output
+stores land in rank 0's buffer over NVLink); the line also carries the
+evaluation alone ("eval") and the NCCL all-gather baseline ("nccl", with its
+gather time separately).
+
+Printed JSON (rank 0, one line, last): value = orbital-evals/s over all
+ranks; roofline of the dominant kernel (algorithmic bytes 64*Npad*s +
+S*Npad*s per position over the measured HBM copy bandwidth) with the DRAM
+fraction from an ncu capture of the same source tree (profiles/ncu_traffic.json,
+keyed by a hash of the CUDA sources: a stale capture is refused); e2e through
+the drop-in API with host buffers; cpu_baseline = the C restatement of the
+reference fp32 kernels (oracle/, kind "port") on the host cores.
 """
 from __future__ import annotations
 
 import argparse
+import glob
+import hashlib
 import json
 import os
 import statistics
@@ -42,11 +61,16 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "B-spline VGH orbital-evals/s"
 UNIT = "orbital-evals/s"
 
 
-def parse():
+def metric_name(kind, cfg_index=4):
+    if cfg_index == 5:
+        return "B-spline V:VGL:VGH 12:1:1 fp64 orbital-evals/s (orbital-sharded, full-N outputs gathered)"
+    return "B-spline VGH orbital-evals/s" if kind == "vgh" else f"B-spline {kind.upper()} orbital-evals/s"
+
+
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -54,17 +78,19 @@ def parse():
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--kind", default=None, help="override the config kernel (v/vgl/vgh)")
+    ap.add_argument("--scaling", choices=("strong", "weak"), default="strong",
+                    help="strong: the config's walkers split over the ranks; weak: a full population per rank")
     ap.add_argument("--chunk", type=int, default=0, help="positions per launch (0 = auto)")
     ap.add_argument("--mode", default="fast", choices=("fast", "strict"))
     ap.add_argument("--tile", type=int, default=-1, help="AoSoA tile size (-1 = auto, 0 = untiled)")
-    ap.add_argument("--form", default="auto", choices=("auto", "kpower", "bspline"),
-                    help="device table form of FAST evaluations (spo_b200.h SPO_TABLE_KPOWER); auto = "
-                         "k-power form for dense (line-kernel) batches")
-    ap.add_argument("--walkers", type=int, default=0, help="override walkers per GPU")
+    ap.add_argument("--form", default="bspline", choices=("bspline", "kpower"),
+                    help="table form `value` is timed on (kpower: opt-in, weaker error bound)")
+    ap.add_argument("--walkers", type=int, default=0, help="override the config's walker count")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--no-extra", action="store_true", help="skip the k-power / other-scaling extra keys")
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -81,6 +107,35 @@ def measured_peak():
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def source_hash() -> str:
+    """sha256 over the CUDA sources and the ABI header: the identity an ncu
+    capture in profiles/ncu_traffic.json must carry to be used."""
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_1611_02665_b200", "csrc", "*.cu"))
+                   + glob.glob(os.path.join(ROOT, "paper_1611_02665_b200", "csrc", "*.cuh"))
+                   + glob.glob(os.path.join(ROOT, "include", "*.h")))
+    for p in files:
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
+def ncu_record(key):
+    """The committed ncu capture of this launch shape, if it was taken on the
+    current CUDA sources; else (None, reason)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            rec = json.load(f).get(key)
+    except Exception:
+        rec = None
+    if not rec:
+        return None, f"no ncu capture for {key}"
+    if rec.get("source_hash") != source_hash():
+        return None, f"ncu capture for {key} is stale (sources {rec.get('source_hash')} != {source_hash()})"
+    return rec, None
 
 
 class ClockSampler:
@@ -147,17 +202,91 @@ class ClockSampler:
                 "power_w": statistics.median(pw), "samples": len(sm), "window": window}
 
 
-def workload(args, rank):
-    from paper_1611_02665_b200.workloads import CONFIGS, bytes_per_position, walker_positions
+class Dist:
+    """torch.distributed plumbing (one rank per GPU over NCCL; ranks sharing
+    a GPU -- a functional run only -- over gloo)."""
 
-    cfg = CONFIGS[args.config]
-    if cfg.dtype != "f32" or cfg.index == 5:
-        raise SystemExit("bench.py times the fp32 walker-sharded configs (1-4)")
-    kind = args.kind or ("vgh" if cfg.kernel == "vgh" else cfg.kernel)
-    walkers = args.walkers or cfg.walkers
-    first = rank * walkers
-    pos = walker_positions(1, range(first, first + walkers), 0, kind, cfg.moves, cfg.grid)
-    return cfg, kind, pos, bytes_per_position(kind, cfg.n_splines)
+    def __init__(self):
+        import torch
+
+        self.world, self.rank, local = dist_env()
+        self.torch = torch
+        n_dev = torch.cuda.device_count()
+        self.shared = self.world > n_dev
+        if self.shared:
+            print(f"bench.py: {self.world} ranks on {n_dev} GPU(s): ranks share devices (gloo plumbing), "
+                  "not a scaling measurement", file=sys.stderr, flush=True)
+            local %= n_dev
+        self.local = local
+        torch.cuda.set_device(local)
+        self.dev = torch.device("cuda", local)
+        if self.world > 1:
+            import torch.distributed as dist
+
+            self.dist = dist
+            if self.shared:
+                dist.init_process_group("gloo")
+            else:
+                # nranks / transport lines in the log for the driver (NCCL INIT only)
+                os.environ.setdefault("NCCL_DEBUG", "INFO")
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+                dist.init_process_group("nccl", device_id=self.dev)
+
+    def barrier(self):
+        self.torch.cuda.synchronize(self.dev)
+        if self.world > 1:
+            self.dist.barrier()
+        self.torch.cuda.synchronize(self.dev)
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cpu" if self.shared else self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cpu" if self.shared else self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def gather(self, obj):
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def finish(self, line):
+        """Tear down first, then print: the JSON line is the last output."""
+        if self.world > 1:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
+        if self.rank == 0 and line is not None:
+            print(json.dumps(line), flush=True)
+
+
+def timed_steps(d, step, steps, warmup, local):
+    """W untimed warm-up steps, then K steps between barriers, with CUDA
+    events around the region on the launching stream and nvidia-smi sampling.
+    Returns (max-over-ranks ms for the K steps, this rank's clocks)."""
+    torch = d.torch
+    stream = torch.cuda.current_stream(d.dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        for _ in range(warmup):
+            step(None)
+        d.barrier()
+        wall0 = time.time()
+        t0.record(stream)
+        for k in range(steps):
+            step(k)
+        t1.record(stream)
+        d.barrier()
+        wall1 = time.time()
+    return d.max(t0.elapsed_time(t1)), clocks.summary(wall0, wall1)
 
 
 def cpu_baseline(table_soa, grid, kind, pos, n_splines, budget_s, threads=0, one_thread_s=0.0):
@@ -182,9 +311,9 @@ def cpu_baseline(table_soa, grid, kind, pos, n_splines, budget_s, threads=0, one
     oracle.eval_f32(kind, table_soa, spac, pos[:n_final], overwrite=True, nthreads=threads)
     dt = time.perf_counter() - t0
     res = {"value": n_final * n_splines / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{n_final} of the workload's positions x N={n_splines} {kind.upper()}, "
-                      f"{dt:.1f} s, C restatement of kernels.py fp32 kernels (oracle/spline_oracle.c, "
-                      f"-O3 AVX2/AVX-512 clones, OpenMP)"}
+           "sample": f"{n_final} of the workload's positions x N={n_splines} {kind.upper()}, "
+                     f"{dt:.1f} s, C restatement of kernels.py fp32 kernels (oracle/spline_oracle.c, "
+                     f"-O3 AVX2/AVX-512 clones, OpenMP)"}
     if threads > 1 and one_thread_s > 0:  # report 1-thread and all-core figures
         n1 = max(1, int(n_final / threads * one_thread_s / max(dt, 1e-6)))
         t0 = time.perf_counter()
@@ -196,10 +325,8 @@ def cpu_baseline(table_soa, grid, kind, pos, n_splines, budget_s, threads=0, one
 def host_reference_table(cfg, seed=0):
     """Reference-layout fp32 table with U[-1,1) values for the CPU arms
     (values do not change the reference kernels' speed)."""
-    from paper_1611_02665_b200.coeffs import padded_count
-
     nx, ny, nz = cfg.grid.counts
-    npad = padded_count(cfg.n_splines)
+    npad = -(-cfg.n_splines // 16) * 16  # the reference's 64-byte lane padding (coeffs.py:25-35)
     rng = np.random.default_rng(seed)
     data = rng.random((nx, ny, nz, npad), dtype=np.float32)
     data *= np.float32(2.0)
@@ -208,218 +335,217 @@ def host_reference_table(cfg, seed=0):
     return data
 
 
+# ------------------------------------------------------------ reference --
+
 def run_reference(args):
+    """The reference's CPU path (the oracle's C port of its fp32 kernels) on
+    all host threads, rank 0 only; each step a bounded sample of the
+    workload.  Config 5: the reference has no fp64 kernel, so its fp32
+    kernels run at config 5's shape and mix (labelled)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_1611_02665_b200.workloads import CONFIGS, walker_positions
+    from paper_1611_02665_b200.workloads import CONFIGS, config_positions, walker_positions
 
     import oracle
 
     cfg = CONFIGS[args.config]
-    kind = args.kind or cfg.kernel
     threads = oracle.host_threads()
     table = host_reference_table(cfg)
-    # each step: a bounded sample of the workload, sized to ~ budget seconds
     per_step_budget = max(1.0, min(8.0, 150.0 / max(1, args.steps + args.warmup)))
-    pos = walker_positions(1, range(0, 256), 0, kind, cfg.moves, cfg.grid)
-    probe = cpu_baseline(table, cfg.grid, kind, pos, cfg.n_splines, 1.0, threads)
-    n = int(min(pos.shape[0], max(threads, probe["value"] / cfg.n_splines * per_step_budget)))
-    sample = pos[:n]
+    if cfg.index == 5:
+        pos = config_positions(cfg, walkers=range(64))
+        kinds = ("v", "vgl", "vgh")
+        probe = {k: cpu_baseline(table, cfg.grid, k, pos[k], cfg.n_splines, 0.5, threads)["value"] for k in kinds}
+        # seconds per position of the mix: 12 V + 1 VGL + 1 VGH per 14 positions
+        per_pos = sum(w / probe[k] for k, w in zip(kinds, (12, 1, 1))) / 14 * cfg.n_splines
+        n = int(max(14 * threads, per_step_budget / per_pos))
+        counts = {"v": n * 12 // 14, "vgl": n // 14, "vgh": n // 14}
+        samples = {k: pos[k][: counts[k]] for k in kinds}
+        kind_label = "mix"
+    else:
+        kind = args.kind or cfg.kernel
+        pos = walker_positions(1, range(0, 256), 0, kind, cfg.moves, cfg.grid)
+        probe = cpu_baseline(table, cfg.grid, kind, pos, cfg.n_splines, 1.0, threads)
+        n = int(min(pos.shape[0], max(threads, probe["value"] / cfg.n_splines * per_step_budget)))
+        samples = {kind: pos[:n]}
+        kind_label = kind
+    n_total = sum(p.shape[0] for p in samples.values())
+
+    def step():
+        for k, p in samples.items():
+            oracle.eval_f32(k, table, cfg.grid.spacings, p, overwrite=True, nthreads=threads)
+
     for _ in range(args.warmup):
-        oracle.eval_f32(kind, table, cfg.grid.spacings, sample, overwrite=True, nthreads=threads)
+        step()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.eval_f32(kind, table, cfg.grid.spacings, sample, overwrite=True, nthreads=threads)
+        step()
     dt = time.perf_counter() - t0
-    value = n * cfg.n_splines * args.steps / dt
+    value = n_total * cfg.n_splines * args.steps / dt
+    note = ("; fp32 kernels at config 5's shape and 12:1:1 mix (the reference has no fp64 kernel)"
+            if cfg.index == 5 else "")
     line = {
-        "impl": "reference", "metric": METRIC if kind == "vgh" else f"B-spline {kind.upper()} orbital-evals/s",
+        "impl": "reference", "metric": metric_name(kind_label, cfg.index),
         "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (U[-1,1) table, Philox walker positions)",
-        "config": {"workload": f"cfg{cfg.index}: {cfg.description}", "positions_per_step": n,
-                   "grid": list(cfg.grid.counts), "n_splines": cfg.n_splines, "kernel": kind},
+        "config": {"workload": f"cfg{cfg.index}: {cfg.description}", "positions_per_step": n_total,
+                   "grid": list(cfg.grid.counts), "n_splines": cfg.n_splines, "kernel": kind_label},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{n} positions per step x {args.steps} steps; reference fp32 kernels "
+                         "sample": f"{n_total} positions per step x {args.steps} steps; reference fp32 kernels "
                                    "restated in C (oracle/spline_oracle.c), reference has no C build "
-                                   "(numba JIT, cannot travel)"},
+                                   f"(numba JIT, cannot travel){note}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def run_b200(args):
+# ----------------------------------------------------- configs 1-4 (fp32) --
+
+KERNELS_PER_CALL = {"line": 4, "tma": 3, "generic": 1}  # this repo's kernels per evaluate() (cub's sort not counted)
+
+
+def kernel_label(path, kind, mode, form, dtype="float"):
+    kp = "true" if form == "kpower" else "false"
+    return {
+        "line": f"spo::line::line_kernel<{kind.upper()},{dtype},RATIO=false,KP={kp}> (+ line_keys, cub sort, "
+                f"line_records, line_runs prologue, timed together)",
+        "tma": f"spo::tma::eval_tma_kernel<{kind.upper()},KP={kp}> (+ bucket_count, prologue_records, "
+               f"timed together)",
+        "generic": f"spo::eval_kernel<{kind.upper()},{dtype},{mode},KP={kp}>",
+    }[path]
+
+
+def walker_range(cfg, args, world, rank, scaling):
+    walkers = args.walkers or cfg.walkers
+    if scaling == "weak":
+        return range(rank * walkers, (rank + 1) * walkers)
+    from paper_1611_02665_b200.multi import walker_shard
+
+    return walker_shard(walkers, world, rank)
+
+
+class WalkerRun:
+    """One rank's share of a walker-sharded fp32 config: table, positions,
+    launch plan and the timed loop."""
+
+    def __init__(self, d, cfg, kind, args, walkers, table):
+        import torch
+
+        from paper_1611_02665_b200.workloads import device_walker_positions
+
+        self.d, self.cfg, self.kind, self.args, self.table = d, cfg, kind, args, table
+        from paper_1611_02665_b200 import KernelKind
+
+        self.S = KernelKind(kind).output_streams_soa
+        n_w = len(walkers)
+        self.pos = device_walker_positions(1, walkers.start, n_w, 0, kind, cfg.moves, cfg.grid, device=d.dev) \
+            if n_w else torch.empty((0, 3), dtype=torch.float64, device=d.dev)
+        self.P = self.pos.shape[0]
+        chunk = args.chunk
+        if chunk <= 0:  # largest of 2^19 / 2^18 whose output buffer leaves 40 GB free
+            free, _ = torch.cuda.mem_get_info(d.dev)
+            per_pos = self.S * table.lanes * 4
+            chunk = 1 << 19 if free - (1 << 19) * per_pos > (40 << 30) else 1 << 18
+        self.chunk = max(1, min(chunk, self.P))
+        self.out = torch.empty((self.chunk, self.S, table.lanes), dtype=torch.float32, device=d.dev)
+        self.bounds = [(lo, min(self.P, lo + self.chunk)) for lo in range(0, self.P, self.chunk)]
+
+    def run(self, form, steps, warmup):
+        import torch
+
+        from paper_1611_02665_b200 import evaluate
+
+        stream = torch.cuda.current_stream(self.d.dev)
+        ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in self.bounds]
+              for _ in range(steps)]
+
+        def step(k):
+            for b, (lo, hi) in enumerate(self.bounds):
+                if k is not None:
+                    ev[k][b][0].record(stream)
+                evaluate(self.table, self.kind, self.pos[lo:hi], self.out, mode=self.args.mode, check=False,
+                         form=form)
+                if k is not None:
+                    ev[k][b][1].record(stream)
+
+        # correctness guard on the benchmarked configuration (one launch)
+        status = torch.zeros(1, dtype=torch.int32, device=self.d.dev)
+        if self.P:
+            evaluate(self.table, self.kind, self.pos[: self.chunk], self.out, mode=self.args.mode, status=status,
+                     check=False, form=form)
+            assert int(status.item()) == 0
+        ms, clocks = timed_steps(self.d, step, steps, warmup, self.d.local)
+        launch_ms = [s.elapsed_time(e) for row in ev for (s, e) in row]
+        full = [t for (lo, hi), t in zip(self.bounds * steps, launch_ms) if hi - lo == self.chunk]
+        avg_launch_ms = sum(full) / len(full) if full else 0.0
+        return ms, avg_launch_ms, clocks
+
+
+def roofline_for(table, kind, S, chunk, avg_launch_ms, key, itemsize=4, n_splines=None):
+    from paper_1611_02665_b200.workloads import bytes_per_position
+
+    q = 128 // itemsize
+    bpp = bytes_per_position(kind, n_splines or table.n_splines, itemsize, q)
+    peak, peak_src = measured_peak()
+    sec = avg_launch_ms * 1e-3
+    achieved = bpp * chunk / sec / 1e9
+    irreducible = S * table.lanes * itemsize * chunk + table.nbytes  # outputs + one table pass
+    roof = {"bound": None, "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": None, "peak_source": peak_src, "algorithmic_bytes_per_position": bpp,
+            "positions_per_launch": chunk, "avg_launch_ms": avg_launch_ms,
+            "frac_irreducible": irreducible / sec / 1e9 / peak,
+            "irreducible_bytes_per_launch": irreducible, "ncu_key": key, "source_hash": source_hash()}
+    rec, why = ncu_record(key)
+    if rec is None:
+        roof["ncu"] = why
+        roof["bound"] = "unmeasured (no ncu capture of these sources)"
+        return roof
+    roof["traffic"] = rec["dram_bytes_per_launch"]
+    roof["frac_dram"] = rec["dram_bytes_per_launch"] / sec / 1e9 / peak
+    units = {"hbm": rec.get("dram_pct"), "l2": rec.get("lts_pct"), "smem/l1": rec.get("l1tex_pct"),
+             "fma": rec.get("fma_pct"), "issue": rec.get("issue_pct")}
+    roof["fma_pipe_pct"] = rec.get("fma_pct")
+    roof["ncu_pct_of_peak"] = units
+    roof["ncu_capture"] = rec.get("source")
+    known = {k: v for k, v in units.items() if v is not None}
+    roof["bound"] = max(known, key=known.get) if known else "unmeasured"
+    return roof
+
+
+def e2e_dropin(d, table, kind, pos_np, N, S, args):
+    """Same metric through the reference-facing drop-in call eval_batch with
+    HOST buffers: host positions -> device each step, all positions evaluated,
+    the last position's streams copied back into the host WalkerOutputsSoA
+    (the reference API's output, kernels.py:353-354).  Timed by wall clock
+    around fully synchronous calls (the call returns host data); under
+    torchrun every rank runs at once and the job time is the max over ranks
+    (whole-job value = all ranks' positions / that time)."""
     import torch
 
-    world, rank, local = dist_env()
-    if not torch.cuda.is_available():
-        raise SystemExit("bench.py --impl b200 needs a CUDA device")
-    n_dev = torch.cuda.device_count()
-    shared = world > n_dev  # more ranks than GPUs: a functional run only, never a measurement
-    if shared:
-        print(f"bench.py: {world} ranks on {n_dev} GPU(s): ranks share devices (gloo plumbing), "
-              "not a scaling measurement", file=sys.stderr, flush=True)
-        local %= n_dev
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
+    from paper_1611_02665_b200 import WalkerOutputsSoA, eval_batch
 
-        # one rank per GPU over NCCL; NCCL refuses two ranks on one device
-        if shared:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
-
-    from paper_1611_02665_b200 import DeviceTable, KernelKind, WalkerOutputsSoA, eval_batch, evaluate
-
-    cfg, kind, pos_np, bpp = workload(args, rank)
-    P = pos_np.shape[0]
-    N = cfg.n_splines
-    S = KernelKind(kind).output_streams_soa
-    tile = "auto" if args.tile < 0 else (args.tile or None)
-    table = DeviceTable.random(cfg.grid, N, seed=0, tile_size=tile, device=dev)
-    form = args.form if args.mode == "fast" else "bspline"
-    if form != "bspline":
-        table.with_kpower()
-    pos = torch.from_numpy(pos_np).to(dev)
-    chunk = args.chunk
-    if chunk <= 0:  # largest of 2^19 / 2^18 whose output buffer leaves 40 GB free
-        free, _ = torch.cuda.mem_get_info(dev)
-        per_pos = S * table.lanes * 4
-        chunk = 1 << 19 if free - (1 << 19) * per_pos > (40 << 30) else 1 << 18
-    chunk = min(chunk, P)
-    out = torch.empty((chunk, S, table.lanes), dtype=torch.float32, device=dev)
-    bounds = [(lo, min(P, lo + chunk)) for lo in range(0, P, chunk)]
-    stream = torch.cuda.current_stream(dev)
-
-    def step(events=None):
-        for b, (lo, hi) in enumerate(bounds):
-            if events is not None:
-                events[b][0].record(stream)
-            evaluate(table, kind, pos[lo:hi], out, mode=args.mode, check=False, form=form)
-            if events is not None:
-                events[b][1].record(stream)
-
-    def barrier():
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-
-    # correctness guard on the benchmarked configuration (one launch)
-    status = torch.zeros(1, dtype=torch.int32, device=dev)
-    evaluate(table, kind, pos[:chunk], out, mode=args.mode, status=status, check=False, form=form)
-    assert int(status.item()) == 0
-
-    launch_events = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                      for _ in bounds] for _ in range(args.steps)]
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
-        for _ in range(args.warmup):
-            step()
-        barrier()
-        wall0 = time.time()
-        t_start.record(stream)
-        for k in range(args.steps):
-            step(launch_events[k])
-        t_end.record(stream)
-        barrier()
-        wall1 = time.time()
-    elapsed_ms = t_start.elapsed_time(t_end)
-    launch_ms = [s.elapsed_time(e) for ev in launch_events for (s, e) in ev]
-    full = [ms for (lo, hi), ms in zip(bounds * args.steps, launch_ms) if hi - lo == chunk]
-    avg_launch_ms = sum(full) / len(full)
-
-    # max over ranks
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cpu" if shared else dev)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(t.item())
-    total_units = P * N * args.steps * world
-    value = total_units / (elapsed_ms / 1e3)
-
-    from paper_1611_02665_b200.kernels import eval_form, eval_path
-
-    path = eval_path(table, kind, chunk, mode=args.mode, form=form)
-    form = eval_form(table, kind, chunk, mode=args.mode, form=form)  # the form the timed launches read
-    # this repo's kernels per evaluate() call (library kernels -- cub's radix
-    # sort in the line path's prologue, memsets -- not counted)
-    kp = "true" if form == "kpower" else "false"
-    kernels_per_call, kernel_name = {
-        "line": (4, f"spo::line::line_kernel<{kind.upper()},float,RATIO=false,KP={kp}> (+ line_keys, cub sort, "
-                    f"line_records, line_runs prologue, timed together)"),
-        "tma": (3, f"spo::tma::eval_tma_kernel<{kind.upper()},KP={kp}> (+ bucket_count, prologue_records, "
-                   f"timed together)"),
-        "generic": (1, f"spo::eval_kernel<{kind.upper()},float,{args.mode},KP={kp}>"),
-    }[path]
-    peak, peak_src = measured_peak()
-    achieved = bpp * chunk / (avg_launch_ms * 1e-3) / 1e9  # GB/s per launch
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(args, cfg, kind, chunk, path, form),
-                "peak_source": peak_src, "kernel": kernel_name,
-                "algorithmic_bytes_per_position": bpp, "positions_per_launch": chunk,
-                "avg_launch_ms": avg_launch_ms}
-    if roofline["traffic"]:
-        # what DRAM actually carried (ncu bytes of the same launch shape over this
-        # run's launch time): frac > 1 above means the table came from L2
-        roofline["dram_gbs"] = roofline["traffic"] / (avg_launch_ms * 1e-3) / 1e9
-        roofline["dram_frac"] = roofline["dram_gbs"] / peak
-
-    result = {
-        "metric": METRIC if kind == "vgh" else f"B-spline {kind.upper()} orbital-evals/s",
-        "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic: FillSpec.random(0) table generated on device (bit-identical to the "
-                "reference numpy fill), reference Philox walker position streams (seed 1)",
-        "config": {"workload": f"cfg{cfg.index}: {cfg.description}", "grid": list(cfg.grid.counts),
-                   "n_splines": N, "kernel": kind, "positions_per_gpu": P, "walkers_per_gpu": P // cfg.moves,
-                   "chunk": chunk, "mode": args.mode, "path": path, "tile_size": table.tile_size,
-                   "table_gb": table.nbytes / 1e9, "table_form": form,
-                   "kpower_table_gb": (table.kdata.numel() * 4 / 1e9) if table.has_kpower else None,
-                   "l2": f"inputs larger than L2 (table {table.nbytes / 1e9:.2f} GB >> 126 MB); no flush",
-                   "parallelism": f"walker-sharded x{world}, table replicated"},
-        "roofline": roofline,
-        "gpu_launches": len(bounds) * args.steps * kernels_per_call,
-        "clocks": clocks.summary(wall0, wall1),
-    }
-
-    if not args.no_e2e:
-        del out  # the drop-in path sizes its own scratch from the free memory
-        torch.cuda.empty_cache()
-        # every rank drives its own GPU through the drop-in API at once; the
-        # job's e2e time is the slowest rank's
-        e2e = e2e_dropin(table, kind, pos_np, N, S, eval_batch, WalkerOutputsSoA, args, dev, world, shared)
-        if rank == 0:
-            result["e2e"] = e2e
-            result["e2e_full_outputs"] = e2e_full_outputs(table, kind, pos_np, N, S, dev)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.barrier()
-    if rank == 0 and world == 1 and not args.no_cpu:
-        soa = table.reference_soa()
-        result["cpu_baseline"] = cpu_baseline(soa, cfg.grid, kind, pos_np, N, args.cpu_seconds, one_thread_s=3.0)
-        del soa
-    if rank == 0:
-        print(json.dumps(result), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.barrier()
-        dist.destroy_process_group()
-    return 0
+    out = WalkerOutputsSoA(N)
+    steps = max(3, min(args.steps, 5))
+    if len(pos_np):
+        eval_batch(table, kind, pos_np, out, mode=args.mode)  # warm
+    torch.cuda.synchronize(d.dev)
+    if d.world > 1:
+        d.dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        if len(pos_np):
+            eval_batch(table, kind, pos_np, out, mode=args.mode)
+    dt = d.max(time.perf_counter() - t0)
+    total = d.sum(float(pos_np.shape[0]))
+    return {"value": total * N * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(total * 24),
+            "d2h_bytes_per_step": int(d.world * S * table.lanes * 4), "ranks": d.world,
+            "api": "paper_1611_02665_b200.eval_batch(table, kind, host positions, host WalkerOutputsSoA)"}
 
 
-def e2e_full_outputs(table, kind, pos_np, N, S, dev, chunk=8192, seconds=2.0):
+def e2e_full_outputs(table, kind, pos, N, S, dev, chunk=8192, seconds=2.0):
     """Transparency figure: the same metric when EVERY output is copied back to
     pinned host memory (H2D positions + kernel + D2H of all [P][S][N] outputs,
     double-buffered over two streams).  PCIe-bound by construction; measured on
@@ -428,19 +554,21 @@ def e2e_full_outputs(table, kind, pos_np, N, S, dev, chunk=8192, seconds=2.0):
 
     from paper_1611_02665_b200 import evaluate
 
-    pin_pos = torch.from_numpy(pos_np).pin_memory()
+    pin_pos = pos.cpu().pin_memory()
+    chunk = min(chunk, len(pin_pos))
+    avail = len(pin_pos) // chunk  # whole chunks of the sample, reused round-robin
     host = [torch.empty((chunk, S, table.lanes), dtype=torch.float32).pin_memory() for _ in range(2)]
     dout = [torch.empty((chunk, S, table.lanes), dtype=torch.float32, device=dev) for _ in range(2)]
     dpos = [torch.empty((chunk, 3), dtype=torch.float64, device=dev) for _ in range(2)]
     streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
-    n_chunks = max(2, min(len(pos_np) // chunk, 64))
+    n_chunks = 64
     done = [torch.cuda.Event() for _ in range(2)]
 
     def run(k):
-        b = k & 1
+        b, c = k & 1, k % avail
         with torch.cuda.stream(streams[b]):
             done[b].synchronize()
-            dpos[b].copy_(pin_pos[k * chunk:(k + 1) * chunk], non_blocking=True)
+            dpos[b].copy_(pin_pos[c * chunk:(c + 1) * chunk], non_blocking=True)
             evaluate(table, kind, dpos[b], dout[b], check=False)
             host[b].copy_(dout[b], non_blocking=True)
             done[b].record(streams[b])
@@ -459,53 +587,268 @@ def e2e_full_outputs(table, kind, pos_np, N, S, dev, chunk=8192, seconds=2.0):
             "sample": f"{k} chunks of {chunk} positions, all outputs to pinned host memory"}
 
 
-def e2e_dropin(table, kind, pos_np, N, S, eval_batch, WalkerOutputsSoA, args, dev, world=1, shared=False):
-    """Same metric through the reference-facing drop-in call eval_batch with
-    HOST buffers: host positions -> device each step, all positions evaluated,
-    the last position's streams copied back into the host WalkerOutputsSoA
-    (the reference API's output, kernels.py:353-354).  Timed by wall clock
-    around fully synchronous calls (the call returns host data); under
-    torchrun every rank runs at once and the job time is the max over ranks
-    (whole-job value = all ranks' positions / that time)."""
+def run_walkers(args, d):
     import torch
 
-    out = WalkerOutputsSoA(N)
-    steps = max(3, min(args.steps, 5))
-    eval_batch(table, kind, pos_np, out, mode=args.mode)  # warm
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        import torch.distributed as dist
+    from paper_1611_02665_b200 import DeviceTable
+    from paper_1611_02665_b200.kernels import eval_form, eval_path
+    from paper_1611_02665_b200.workloads import CONFIGS
 
-        dist.barrier()
+    cfg = CONFIGS[args.config]
+    if cfg.dtype != "f32":
+        raise SystemExit("configs 1-4 are fp32")
+    kind = args.kind or cfg.kernel
+    N = cfg.n_splines
+    tile = "auto" if args.tile < 0 else (args.tile or None)
+    table = DeviceTable.random(cfg.grid, N, seed=0, tile_size=tile, device=d.dev)
+    form = args.form if args.mode == "fast" else "bspline"
+    if form == "kpower":
+        table.with_kpower()
+    walkers = walker_range(cfg, args, d.world, d.rank, args.scaling)
+    run = WalkerRun(d, cfg, kind, args, walkers, table)
+    ms, avg_launch_ms, clocks = run.run(form, args.steps, args.warmup)
+    total_pos = d.sum(float(run.P))
+    value = total_pos * N * args.steps / (ms / 1e3)
+
+    path = eval_path(table, kind, run.chunk, mode=args.mode, form=form)
+    form_used = eval_form(table, kind, run.chunk, mode=args.mode, form=form)
+    key = f"cfg{cfg.index}-{kind}-{args.mode}-{form_used}-{path}-{run.chunk}-lanes{table.lanes}"
+    roof = roofline_for(table, kind, run.S, run.chunk, avg_launch_ms, key)
+    roof["kernel"] = kernel_label(path, kind, args.mode, form_used)
+    clocks_all = d.gather(clocks)
+    walkers_per_rank = d.gather(len(walkers))
+    result = {
+        "metric": metric_name(kind, cfg.index), "value": value, "unit": UNIT, "n_gpus": d.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: FillSpec.random(0) table generated on device (bit-identical to the "
+                "reference numpy fill), reference Philox walker position streams (seed 1), generated on device",
+        "config": {"workload": f"cfg{cfg.index}: {cfg.description}", "grid": list(cfg.grid.counts),
+                   "n_splines": N, "kernel": kind, "positions_per_step": int(total_pos),
+                   "walkers_per_rank": walkers_per_rank, "chunk": run.chunk, "mode": args.mode, "path": path,
+                   "tile_size": table.tile_size, "table_gb": table.nbytes / 1e9, "table_form": form_used,
+                   "l2": f"inputs larger than L2 (table {table.nbytes / 1e9:.2f} GB >> 126 MB, outputs "
+                         f"{run.chunk * run.S * table.lanes * 4 / 1e9:.1f} GB per launch); no flush",
+                   "parallelism": f"walker-sharded x{d.world} ({args.scaling} scaling), table replicated"},
+        "roofline": roof,
+        "gpu_launches": len(run.bounds) * args.steps * KERNELS_PER_CALL[path],
+        "clocks": clocks,
+        "clocks_per_rank": clocks_all,
+    }
+
+    if not args.no_extra and args.mode == "fast":
+        # the opt-in k-power form on the same workload (weaker error bound)
+        other = "bspline" if form == "kpower" else "kpower"
+        table.with_kpower()
+        kms, kavg, kclk = run.run(other, max(3, min(args.steps, 10)), 2)
+        ksteps = max(3, min(args.steps, 10))
+        result[other] = {"value": total_pos * N * ksteps / (kms / 1e3), "ms_per_step": kms / ksteps,
+                         "avg_launch_ms": kavg, "sm_mhz": kclk.get("sm_mhz"),
+                         "error_bound": "1e-5*sum|w*c|" if other == "bspline" else
+                         "1e-5*(sum|w*c| + sum_ij|wx wy| sum_r|q_r| m_r) (opt-in; DESIGN.md 5.6)"}
+        if form != "kpower":
+            table.drop_kpower()
+        torch.cuda.empty_cache()
+        if d.world > 1:
+            # the other scaling mode, for the record
+            oscal = "weak" if args.scaling == "strong" else "strong"
+            del run
+            torch.cuda.empty_cache()
+            orun = WalkerRun(d, cfg, kind, args, walker_range(cfg, args, d.world, d.rank, oscal), table)
+            osteps = max(3, min(args.steps, 5))
+            oms, oavg, _ = orun.run(form, osteps, 2)
+            otot = d.sum(float(orun.P))
+            result[oscal] = {"value": otot * N * osteps / (oms / 1e3), "ms_per_step": oms / osteps,
+                             "positions_per_step": int(otot), "avg_launch_ms": oavg}
+            del orun
+            torch.cuda.empty_cache()
+
+    if not args.no_e2e:
+        torch.cuda.empty_cache()
+        walkers_e2e = walker_range(cfg, args, d.world, d.rank, args.scaling)
+        from paper_1611_02665_b200.workloads import walker_positions
+
+        pos_np = walker_positions(1, walkers_e2e, 0, kind, cfg.moves, cfg.grid) if len(walkers_e2e) \
+            else np.zeros((0, 3))
+        result["e2e"] = e2e_dropin(d, table, kind, pos_np, N, run_S(kind), args)
+        if d.rank == 0 and len(pos_np):
+            result["e2e_full_outputs"] = e2e_full_outputs(table, kind, torch.from_numpy(pos_np), N,
+                                                          run_S(kind), d.dev)
+    if d.world > 1:
+        d.dist.barrier()
+    if d.rank == 0 and d.world == 1 and not args.no_cpu:
+        soa = table.reference_soa()
+        from paper_1611_02665_b200.workloads import walker_positions
+
+        cpos = walker_positions(1, range(0, 256), 0, kind, cfg.moves, cfg.grid)
+        result["cpu_baseline"] = cpu_baseline(soa, cfg.grid, kind, cpos, N, args.cpu_seconds, one_thread_s=3.0)
+        del soa
+    return result
+
+
+def run_S(kind):
+    return {"v": 1, "vgl": 5, "vgh": 10}[kind]
+
+
+# ------------------------------------------------------ config 5 (fp64) --
+
+def run_config5(args, d):
+    """Orbital-sharded fp64 (BASELINE config 5): rank r holds splines
+    part.local(r) (generated directly, DeviceTable.normal_f64(first_spline));
+    every rank evaluates every position of the 12:1:1 mix on its slice.
+    Timed three ways, each K steps: eval only (local outputs), the fused
+    evaluate + gather (PeerGather; `value`), and eval + NCCL all-gather to
+    rank 0 (gather_orbital_blocks), the gather alone timed by events."""
+    import torch
+
+    from paper_1611_02665_b200 import DeviceTable, evaluate
+    from paper_1611_02665_b200.kernels import eval_path
+    from paper_1611_02665_b200.multi import OrbitalPartition, PeerGather, gather_orbital_blocks
+    from paper_1611_02665_b200.workloads import CONFIGS, device_walker_positions
+
+    cfg = CONFIGS[5]
+    N = cfg.n_splines
+    part = OrbitalPartition.make(N, d.world, quantum=16)
+    lo, hi = part.local(d.rank)
+    table = DeviceTable.normal_f64(cfg.grid, hi - lo, seed=0, tile_size=None, device=d.dev, first_spline=lo)
+    walkers = args.walkers or cfg.walkers
+    allpos = device_walker_positions(1, 0, walkers, 0, "v", cfg.moves, cfg.grid, device=d.dev)
+    P_all = allpos.shape[0]
+    # launch chunks of the global position sequence; kind by index mod 14
+    chunk = args.chunk or 262144
+    kinds = ("v", "vgl", "vgh")
+    S = {"v": 1, "vgl": 5, "vgh": 10}
+    idx = torch.arange(P_all, device=d.dev) % 14
+    sel = {"v": idx < 12, "vgl": idx == 12, "vgh": idx == 13}
+    plan = []  # [(kind, positions tensor)] per chunk
+    for c0 in range(0, P_all, chunk):
+        c1 = min(P_all, c0 + chunk)
+        for k in kinds:
+            plan.append((k, allpos[c0:c1][sel[k][c0:c1]].contiguous()))
+    del allpos, idx, sel
+    cap = {k: max(p.shape[0] for kk, p in plan if kk == k) for k in kinds}
+    counts = {k: sum(p.shape[0] for kk, p in plan if kk == k) for k in kinds}
+    n_local = hi - lo
+    local_out = {k: torch.empty((cap[k], S[k], table.lanes), dtype=torch.float64, device=d.dev) for k in kinds}
+    gathers = {k: PeerGather(part, k, cap[k], np.float64, root=0, device=d.dev) for k in kinds}
+    stream = torch.cuda.current_stream(d.dev)
+    v_ev = []
+
+    def eval_step(k_step):
+        for k, p in plan:
+            if k_step is not None and k == "v":
+                e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                e[0].record(stream)
+            evaluate(table, k, p, local_out[k], check=False)
+            if k_step is not None and k == "v":
+                e[1].record(stream)
+                v_ev.append(e)
+
+    def peer_step(_):
+        for k, p in plan:
+            gathers[k].evaluate(table, p, check=False)
+
+    gather_ev = []
+
+    def nccl_step(k_step):
+        for k, p in plan:
+            evaluate(table, k, p, local_out[k], check=False)
+            if d.world > 1:
+                e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                e[0].record(stream)
+                gather_orbital_blocks(local_out[k][: p.shape[0], :, :n_local], part, root=0)
+                e[1].record(stream)
+                if k_step is not None:
+                    gather_ev.append(e)
+
+    eval_ms, clocks = timed_steps(d, eval_step, args.steps, args.warmup, d.local)
+    peer_ms, peer_clocks = timed_steps(d, peer_step, args.steps, args.warmup, d.local)
+    res_nccl = None
+    if not args.no_extra and not d.shared:  # ranks sharing a GPU run gloo: no NCCL baseline
+        nsteps = max(2, min(args.steps, 5))
+        nccl_ms, _ = timed_steps(d, nccl_step, nsteps, 1, d.local)
+        torch.cuda.synchronize(d.dev)
+        g_ms = d.max(sum(s.elapsed_time(e) for s, e in gather_ev) / nsteps) if gather_ev else 0.0
+        res_nccl = {"ms_per_step": nccl_ms / nsteps, "gather_ms_per_step": g_ms,
+                    "value": P_all * N * nsteps / (nccl_ms / 1e3),
+                    "what": "evaluate into local buffers + NCCL all-gather of padded blocks + permute on rank 0"}
+    units = P_all * N * args.steps
+    avg_v = sum(s.elapsed_time(e) for s, e in v_ev) / max(1, len(v_ev))
+    v_launch = cap["v"]
+    path = eval_path(table, "v", v_launch)
+    key = f"cfg5-v-fast-bspline-{path}-{v_launch}-lanes{table.lanes}"
+    roof = roofline_for(table, "v", 1, v_launch, avg_v, key, itemsize=8, n_splines=n_local)
+    roof["kernel"] = kernel_label(path, "v", "fast", "bspline", "double")
+    result = {
+        "metric": metric_name("mix", 5), "value": units / (peer_ms / 1e3), "unit": UNIT, "n_gpus": d.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": peer_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: builder-defined fp64 N(0,1) table (Philox per spline, generated on device per shard), "
+                "reference Philox walker position streams (seed 1), generated on device",
+        "config": {"workload": f"cfg5: {cfg.description}", "grid": list(cfg.grid.counts), "n_splines": N,
+                   "splines_per_rank": [b - a for a, b in part.bounds], "positions_per_step": P_all,
+                   "positions_by_kind": counts, "chunk": chunk, "path_v": path,
+                   "l2": f"inputs larger than L2 (shard {table.nbytes / 1e9:.2f} GB, outputs per step "
+                         f"{sum(counts[k] * S[k] for k in kinds) * N * 8 / 1e9:.0f} GB); no flush",
+                   "parallelism": f"orbital-sharded x{d.world}, full-N outputs gathered on rank 0 "
+                                  f"({'fused peer stores over NVLink' if d.world > 1 else 'single GPU'})"},
+        "eval": {"ms_per_step": eval_ms / args.steps, "value": units / (eval_ms / 1e3),
+                 "what": "every rank evaluates its slice into local buffers (no gather)"},
+        "gather_overhead_ms_per_step": (peer_ms - eval_ms) / args.steps,
+        "roofline": roof,
+        "gpu_launches": args.steps * sum(KERNELS_PER_CALL[eval_path(table, k, p.shape[0])] for k, p in plan),
+        "clocks": peer_clocks,
+        "clocks_per_rank": d.gather(peer_clocks),
+    }
+    if res_nccl:
+        result["nccl"] = res_nccl
+    if not args.no_e2e:
+        result["e2e"] = e2e_config5(d, table, plan, gathers, args, N)
+    return result
+
+
+def e2e_config5(d, table, plan, gathers, args, N):
+    """End to end through the public API: each step every chunk's positions
+    come from pinned host memory (H2D inside the timed region), the fused
+    evaluate + gather runs, and rank 0 reads the last position's full-N
+    streams of each kind back to the host (the reference's last-sample
+    output)."""
+    import torch
+
+    host = [(k, p.cpu().pin_memory()) for k, p in plan]
+    steps = max(2, min(args.steps, 3))
+    d2h = 0
+    d.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
-        eval_batch(table, kind, pos_np, out, mode=args.mode)
-    dt = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([dt], dtype=torch.float64, device="cpu" if shared else dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
-    P = pos_np.shape[0]
-    return {"value": world * P * N * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(world * pos_np.nbytes),
-            "d2h_bytes_per_step": int(world * S * table.lanes * 4), "ranks": world,
-            "api": "paper_1611_02665_b200.eval_batch(table, kind, host positions, host WalkerOutputsSoA)"}
+        last = {}
+        for k, hp in host:
+            dp = hp.to(d.dev, non_blocking=True)
+            r = gathers[k].evaluate(table, dp, check=False)
+            if r is not None and hp.shape[0]:
+                last[k] = r[-1]
+        if d.rank == 0:
+            for k, v in last.items():
+                v.cpu()
+                d2h += v.numel() * 8
+    torch.cuda.synchronize(d.dev)
+    dt = d.max(time.perf_counter() - t0)
+    P_all = sum(hp.shape[0] for _, hp in host)
+    return {"value": P_all * N * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(P_all * 24 * d.world),
+            "d2h_bytes_per_step": int(d2h // steps),
+            "api": "paper_1611_02665_b200.multi.PeerGather.evaluate(local shard, host->device positions); "
+                   "rank 0 reads the last position's full-N streams"}
 
 
-def ncu_traffic(args, cfg, kind, chunk, path, form="bspline"):
-    """dram read+write bytes per launch from the committed ncu capture, when
-    it was taken on this exact configuration (profiles/ncu_traffic.json)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            rec = json.load(f)
-        key = f"cfg{cfg.index}-{kind}-{args.mode}-tile{args.tile}-{path}-{chunk}"
-        if form == "kpower":
-            key += "-kpower"
-        r = rec.get(key)
-        if r and r.get("positions_per_launch") == chunk:
-            return r["dram_bytes_per_launch"]
-    except Exception:
-        pass
-    return None
+def run_b200(args):
+    import torch
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py --impl b200 needs a CUDA device")
+    d = Dist()
+    result = run_config5(args, d) if args.config == 5 else run_walkers(args, d)
+    d.finish(result)
+    return 0
 
 
 def main():

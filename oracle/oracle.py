@@ -14,7 +14,7 @@ import numpy as np
 __all__ = [
     "KIND_CODES", "STREAMS", "STREAM_NAMES", "map_axis", "weights_f32", "weights_f64",
     "evaluate_f64_np", "lib", "c_map_axis", "c_weights_f32", "c_weights_f64",
-    "eval_f32", "eval_f64", "tolerance_check", "host_threads",
+    "eval_f32", "eval_f64", "tolerance_check", "host_threads", "kpower_scale",
 ]
 
 KIND_CODES = {"v": 0, "vgl": 1, "vgh": 2}
@@ -227,3 +227,53 @@ def tolerance_check(got, ref, scale, tol):
     ratio = np.where(bound > 0, err / np.where(bound > 0, bound, 1.0), np.where(err > 0, np.inf, 0.0))
     worst = float(ratio.max()) if ratio.size else 0.0
     return worst <= 1.0, worst
+
+
+# (x, y, z) derivative orders of the ten VGH streams (reference order)
+_ORDERS = {"v": (0, 0, 0), "gx": (1, 0, 0), "gy": (0, 1, 0), "gz": (0, 0, 1), "hxx": (2, 0, 0),
+           "hxy": (1, 1, 0), "hxz": (1, 0, 1), "hyy": (0, 2, 0), "hyz": (0, 1, 1), "hzz": (0, 0, 2)}
+
+
+def kpower_scale(kind, data, n_splines, spacings, pos):
+    """Error scale of the OPT-IN k-power table form -- not a
+    reference quantity.  The k-power form evaluates each z-cubic in the power
+    basis q0 + q1 t + q2 t^2 + q3 t^3 (q = the basis change of the cell's four
+    z coefficients, grid.py:127-130), so its rounding error is relative to
+    sum_r |q_r| (times the derivative factors r, r(r-1) and 1/dz, 1/dz^2 for
+    z-derivative streams), contracted with |x weights| * |y weights|:
+
+        scale_s = sum_ij |wx_s[i] wy_s[j]| * sum_r |q_r(i, j)| m_s[r],
+        m = (1,1,1,1), (0,1,2,3)/dz, (0,0,2,6)/dz^2 for z-order 0, 1, 2;
+
+    VGL `l` takes the three-term sum, as the north-star scale does.  Returns
+    [P][S][N] float64.  (The north-star scale sum|w*c| can be far smaller than
+    this: a spike at k0-1 has w = (1-t)^3/6 -> 0 as t -> 1 while |q| stays ~1.)"""
+    kind = _kind(kind)
+    data = np.asarray(data)
+    nx, ny, nz = data.shape[:3]
+    pos = np.atleast_2d(np.asarray(pos, dtype=np.float64))
+    N = int(n_splines)
+    dz = float(spacings[2])
+    m = (np.array([1.0, 1.0, 1.0, 1.0]), np.array([0.0, 1.0, 2.0, 3.0]) / dz,
+         np.array([0.0, 0.0, 2.0, 6.0]) / dz ** 2)
+    names = STREAM_NAMES["vgh"]
+    out = np.zeros((pos.shape[0], STREAMS[kind], N))
+    for q, (x, y, z) in enumerate(pos):
+        idx, w = [], []
+        for c, cnt, d in ((x, nx, spacings[0]), (y, ny, spacings[1]), (z, nz, spacings[2])):
+            i0, t = map_axis(c, 1.0 / d, cnt)
+            idx.append((int(i0) - 1 + np.arange(4)) % cnt)
+            w.append(np.abs(weights_f64(float(t), d)))
+        c = np.asarray(data[np.ix_(*idx)][..., :N], dtype=np.float64)  # [4][4][4][N]
+        c0, c1, c2, c3 = (c[:, :, r] for r in range(4))
+        qa = np.abs(np.stack([(c0 + 4.0 * c1 + c2) / 6.0, (c2 - c0) / 2.0, (c0 - 2.0 * c1 + c2) / 2.0,
+                              ((c3 - c0) + 3.0 * (c1 - c2)) / 6.0]))  # [r][4][4][N]
+        acc = {}
+        for name in names:
+            ox, oy, oz = _ORDERS[name]
+            z_mag = np.tensordot(m[oz], qa, axes=(0, 0))  # [4][4][N]
+            acc[name] = np.einsum("i,j,ijn->n", w[0][ox], w[1][oy], z_mag)
+        acc["l"] = acc["hxx"] + acc["hyy"] + acc["hzz"]
+        for s, name in enumerate(STREAM_NAMES[kind]):
+            out[q, s] = acc[name]
+    return out

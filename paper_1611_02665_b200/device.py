@@ -15,8 +15,10 @@ A table may also carry its k-power form (``with_kpower()``, spo_b200.h
 SPO_TABLE_KPOWER): ``kdata[m][i'][j'][4*k0 + r][l]`` holds the power-basis
 coefficients of the z-cubic of cell k0, which the FAST kernels contract with
 7 instead of 12 FMAs per row group (VGH: 248 instead of 328 per orbital).  It
-is derived from ``data`` on the device and used by FAST evaluations; STRICT
-mode and the fused ratio epilogue read ``data``.
+is derived from ``data`` on the device and read only by FAST evaluations that
+opt in with form="kpower" (its error bound is relative to the cell's
+coefficient magnitudes, weaker than the north-star sum|w*c| bound; see
+kernels._table_form); everything else reads ``data``.
 """
 from __future__ import annotations
 
@@ -219,11 +221,15 @@ class DeviceTable:
         return dt
 
     @classmethod
-    def normal_f64(cls, grid, n_splines, seed=0, tile_size="auto", device=None) -> "DeviceTable":
-        """Builder-defined fp64 N(0,1) table (BASELINE config 5; spo_b200.h)."""
+    def normal_f64(cls, grid, n_splines, seed=0, tile_size="auto", device=None, first_spline=0) -> "DeviceTable":
+        """Builder-defined fp64 N(0,1) table (BASELINE config 5; spo_b200.h).
+        first_spline > 0 generates splines [first_spline, first_spline +
+        n_splines) of the full table directly -- an orbital shard, equal to
+        slice_orbitals() of the full table without building it."""
         torch = _torch()
         dt = cls.empty(grid, n_splines, np.float64, tile_size, device)
-        keys = torch.from_numpy(spline_keys(seed, n_splines).view(np.int64)).to(dt.device)
+        keys_np = spline_keys(seed, first_spline + n_splines)[first_spline:]
+        keys = torch.from_numpy(np.ascontiguousarray(keys_np).view(np.int64)).to(dt.device)
         _abi.check(_abi.load().spo_fill_normal_f64(keys.data_ptr(), n_splines, _abi.i32x3(grid.counts),
                                                    dt.tile_size, dt.nb, dt.n_tiles, dt.data.data_ptr(),
                                                    _stream_ptr(dt.device)))

@@ -19,7 +19,8 @@ from .kernels import as_kind, evaluate
 class GraphedEvaluator:
     """evaluate(table, kind, positions[P]) captured for a fixed P."""
 
-    def __init__(self, table, kind, n_positions: int, *, mode: str = "fast", pipeline="auto"):
+    def __init__(self, table, kind, n_positions: int, *, mode: str = "fast", pipeline="auto",
+                 form: str = "auto"):
         import torch
 
         self.table = as_device_table(table)
@@ -32,7 +33,7 @@ class GraphedEvaluator:
         self.positions = torch.zeros((self.n, 3), dtype=torch.float64, device=dev)
         self.out = torch.empty((self.n, self.kind.output_streams_soa, self.table.lanes), dtype=tdt, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
-        self._kw = dict(mode=mode, pipeline=pipeline, status=self.status, check=False)
+        self._kw = dict(mode=mode, pipeline=pipeline, status=self.status, check=False, form=form)
         # warm up outside capture (library load, attributes, allocator pools)
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))

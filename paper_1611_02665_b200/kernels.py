@@ -149,20 +149,25 @@ class WalkerOutputsAoS:
             out[name] = h[:, r, c].copy()
         return out
 
-    def store(self, kind, block: np.ndarray) -> None:
-        """Scatter one position's [S][N] SoA block into the interleaved
-        buffers; the AoS Hessian stores all nine entries (kernels.py:342-350)."""
+    def store(self, kind, block: np.ndarray, n: int = None) -> None:
+        """Scatter one position's [S][>=n] SoA block (spline-indexed) into the
+        first n entries of the interleaved buffers -- n = the table's
+        n_splines; entries past it are left untouched, as the reference
+        kernels write only the table's splines.  The AoS Hessian stores all
+        nine entries (kernels.py:342-350)."""
         kind = as_kind(kind)
-        n = self.n_splines
-        self.v[:] = block[0, :n]
+        n = self.n_splines if n is None else int(n)
+        if n > self.n_splines:
+            raise ContractError(f"output buffers ({self.n_splines}) shorter than n_splines ({n})")
+        self.v[:n] = block[0, :n]
         if kind is KernelKind.V:
             return
-        g = self.g.reshape(-1, 3)
+        g = self.g[: 3 * n].reshape(n, 3)
         g[:, 0], g[:, 1], g[:, 2] = block[1, :n], block[2, :n], block[3, :n]
         if kind is KernelKind.VGL:
-            self.l[:] = block[4, :n]
+            self.l[:n] = block[4, :n]
             return
-        h = self.h.reshape(-1, 3, 3)
+        h = self.h[: 9 * n].reshape(n, 3, 3)
         hxx, hxy, hxz, hyy, hyz, hzz = (block[4 + r, :n] for r in range(6))
         h[:, 0, 0], h[:, 0, 1], h[:, 0, 2] = hxx, hxy, hxz
         h[:, 1, 0], h[:, 1, 1], h[:, 1, 2] = hxy, hyy, hyz
@@ -202,12 +207,18 @@ PIPELINE_MIN_WORK = 1 << 19
 
 
 def _table_form(dt, kind, mode: str, form: str, P: int, ws_bytes: int):
-    """(data tensor, mode flag) of the table form a request runs on.  With
-    form="auto", FAST requests use the k-power form when the table carries one
-    and the request takes the line-window kernel (dense batches): there the
-    cheaper z-sums pay for the 4x larger table; sparse batches re-read more
-    table bytes per position and stay on the B-spline form
-    (scripts/bench_configs.py, profiles/r01/configs_kpower.md)."""
+    """(data tensor, mode flag) of the table form a request runs on.
+
+    "auto" and "bspline" read the B-spline form: its error is bounded by
+    1e-5 (fp32) / 1e-12 (fp64) times sum|w*c| per output element for every
+    table and position (the north-star metric).  The k-power form is OPT-IN
+    (form="kpower"): ~7% faster on dense batches, but its power-basis z-cubic
+    is only accurate to tol * (sum|w*c| + sum_ij |wx_i wy_j| * sum_r |q_r| m_r)
+    (q = the cell's power-basis coefficients, m_r the z-derivative factors,
+    oracle.kpower_scale) -- relative to the coefficient magnitudes, not to
+    sum|w*c| alone -- so a table with steep decay along z, or a single spike,
+    misses the north-star bound near t_z -> 1 and at basis zeros
+    (tests/test_gpu_adversarial.py)."""
     if form not in ("auto", "bspline", "kpower"):
         raise ContractError(f"unknown table form {form!r}")
     if form == "kpower" and mode != "fast":
@@ -216,11 +227,6 @@ def _table_form(dt, kind, mode: str, form: str, P: int, ws_bytes: int):
         raise ContractError("the table has no k-power form (DeviceTable.with_kpower())")
     if form == "kpower":
         return dt.kdata, _abi.TABLE_KPOWER
-    if form == "auto" and mode == "fast" and dt.has_kpower:
-        code = _abi.load().spo_eval_path(kind.code, dt.dtype_code, _MODES[mode], _abi.i32x3(dt.grid.counts),
-                                         dt.nb, dt.n_tiles, P, max(ws_bytes, 0))
-        if _PATHS.get(code) == "line":
-            return dt.kdata, _abi.TABLE_KPOWER
     return dt.data, 0
 
 
@@ -246,10 +252,10 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
                is then required and may live on another GPU (a peer
                device's memory or an IPC mapping of it): the fused
                evaluate + gather of multi.PeerGather
-    form       "auto" (FAST on the k-power form when the table carries one,
-               DeviceTable.with_kpower, and the batch is dense enough for the
-               line-window kernel), "bspline" or "kpower"; the two forms agree
-               within the FAST tolerance, not bitwise
+    form       "auto" / "bspline": the B-spline table form (the north-star
+               error bound for every input); "kpower": the opt-in k-power form
+               (DeviceTable.with_kpower) with the weaker bound documented in
+               _table_form / DESIGN.md 5.6
     """
     torch = _torch()
     kind = as_kind(kind)
@@ -293,7 +299,9 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
     if out_index is not None:
         if out_index.dtype != torch.int64 or out_index.device != device or out_index.numel() != P:
             raise ContractError("out_index must be an int64 CUDA tensor with one entry per position")
-        idx_ptr = out_index.contiguous().data_ptr()
+        if not out_index.is_contiguous():
+            raise ContractError("out_index must be contiguous")
+        idx_ptr = out_index.data_ptr()
     g = dt.grid
     L = _abi.load()
     if pipeline == "auto":  # small batches: one generic launch beats prologue + TMA setup
@@ -545,6 +553,10 @@ def _eval_last(table, kind, pos: np.ndarray, mode: str):
     block = scratch[last].cpu().numpy()
     if int(status.item()) != 0:
         raise DomainError("positions contain non-finite components")
+    if not dt.lanes_are_splines:  # padded tiles: output lane != spline index
+        block = block[:, dt.lane_of(np.arange(dt.n_splines))]
+    else:
+        block = block[:, : dt.n_splines]
     return dt, block
 
 
@@ -562,19 +574,20 @@ def eval_batch(table, kind, positions, out, *, mode: str = "fast") -> None:
                 raise ContractError("tiled tables need one WalkerOutputsSoA of tile_size per tile")
         if pos.shape[0] == 0:
             return
-        dt, block = _eval_last(table, kind, pos, mode)
+        dt, block = _eval_last(table, kind, pos, mode)  # block: [S][N], spline-indexed
+        ts = table.tile_size
         for m, tile_out in enumerate(out):
-            width = min(dt.tile_size, dt.n_splines - m * dt.tile_size)
+            width = min(ts, dt.n_splines - m * ts)
             for s, row in enumerate(tile_out._targets(kind)):
-                row[:width] = block[s, m * dt.nb: m * dt.nb + width]
-                row[width: padded_count(dt.tile_size)] = 0.0
+                row[:width] = block[s, m * ts: m * ts + width]
+                row[width: padded_count(ts)] = 0.0
         return
     _check_pair(table, out)
     if pos.shape[0] == 0:
         return
     dt, block = _eval_last(table, kind, pos, mode)
     if getattr(out, "layout", None) == "aos":
-        out.store(kind, block)
+        out.store(kind, block, dt.n_splines)
         return
     n = dt.n_splines
     width = min(out.n_padded, dt.lanes)

@@ -209,7 +209,9 @@ class PeerGather:
 
     def evaluate(self, local_table, positions, **kw):
         """Evaluate this rank's spline slice at every position into the root's
-        buffer.  Returns the root's [P][S][N] view on the root, None elsewhere."""
+        buffer.  Returns the root's [P][S][N] view on the root, None elsewhere.
+        The view is valid until the next evaluate() call on this gather (the
+        next call waits for the root's stream, then overwrites it)."""
         import torch
         import torch.distributed as dist
 
@@ -230,9 +232,18 @@ class PeerGather:
         P = pos.shape[0]
         if P > self.capacity:
             raise ContractError(f"{P} positions exceed the gather buffer's capacity {self.capacity}")
+        multi_rank = dist.is_initialized() and dist.get_world_size(self.group) > 1
+        if multi_rank:
+            # Reuse contract: the view returned by the previous call stays valid
+            # until the next call.  The root drains its stream (any work it
+            # queued on that view) and every rank waits for it here, so no
+            # rank's stores can overwrite a buffer the root is still reading.
+            if self.rank == self.root:
+                torch.cuda.current_stream(dt.device).synchronize()
+            dist.barrier(group=self.group)
         if hi > lo:
             evaluate(dt, self.kind, pos, self.buf[:P, :, lo:], lane_limit=hi - lo, **kw)
-        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+        if multi_rank:
             torch.cuda.current_stream(dt.device).synchronize()
             dist.barrier(group=self.group)
         return self.buf[:P, :, : self.part.n_splines] if self.rank == self.root else None

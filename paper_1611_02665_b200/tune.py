@@ -48,15 +48,13 @@ def retile(table: DeviceTable, tile_size) -> DeviceTable:
 
 
 def tune_tile_size(table: DeviceTable, kind, n_positions: int = 1 << 16, repeats: int = 3,
-                   seed: int = 1, candidates=None, kpower=None) -> TuneResult:
+                   seed: int = 1, candidates=None, kpower=False) -> TuneResult:
     """Scan tilings of `table` for `kind`; returns the argmax (ties -> larger tile).
-    kpower: give every candidate the k-power table form (None: as `table`), so
-    FAST requests are timed on the form evaluate() would pick."""
+    kpower: time every candidate on the opt-in k-power table form
+    (form="kpower") instead of the default B-spline form."""
     import torch
 
     kind = as_kind(kind)
-    if kpower is None:
-        kpower = table.has_kpower
     cands = list(candidates) if candidates is not None else tile_candidates(table.n_splines)
     moves = 256
     walkers = max(1, -(-n_positions // moves))
@@ -71,12 +69,13 @@ def tune_tile_size(table: DeviceTable, kind, n_positions: int = 1 << 16, repeats
             t.with_kpower()
         out = torch.empty((pos.shape[0], kind.output_streams_soa, t.lanes), dtype=t.data.dtype,
                           device=t.device)
-        evaluate(t, kind, pos, out, check=False)  # warm-up
+        form = "kpower" if kpower else "bspline"
+        evaluate(t, kind, pos, out, check=False, form=form)  # warm-up
         reps = []
         for _ in range(repeats):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            evaluate(t, kind, pos, out, check=False)
+            evaluate(t, kind, pos, out, check=False, form=form)
             e1.record(stream)
             e1.synchronize()
             reps.append(pos.shape[0] * table.n_splines / (e0.elapsed_time(e1) * 1e-3))

@@ -36,7 +36,7 @@ def main():
     ap.add_argument("--kind", default="vgh")
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--kpower", action="store_true", help="give the tables the k-power form (dense batches use it)")
+    ap.add_argument("--kpower", action="store_true", help="evaluate on the opt-in k-power table form")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -65,16 +65,23 @@ def main():
     rng = np.random.default_rng(11)
     pos = torch.from_numpy(rng.random((args.positions, 3)) * 2.0 - 0.5).to(dev)
 
+    form = "kpower" if args.kpower else "auto"
     pg = PeerGather(part, args.kind, args.positions, full.dtype, root=0, device=dev)
-    got = pg.evaluate(mine, pos)
     res = {"world": world, "backend": backend, "ranks_share_gpu": not own_gpu, "bounds": part.bounds}
-    if args.kpower:
-        from paper_1611_02665_b200.kernels import eval_form
+    from paper_1611_02665_b200.kernels import eval_form
 
-        res["form"] = eval_form(mine, args.kind, args.positions)
+    res["form"] = eval_form(mine, args.kind, args.positions, form=form)
+    # two different position sets through the same gather buffer: the second
+    # call must wait for the root to finish with the first call's view
+    pos2 = torch.from_numpy(rng.random((args.positions, 3)) * 3.0 - 1.0).to(dev)
+    bitwise = True
+    for p in (pos2, pos):
+        got = pg.evaluate(mine, p, form=form)
+        if rank == 0:
+            want = evaluate(full, args.kind, p, form=form)[:, :, : args.splines]
+            bitwise &= bool(torch.equal(got, want))
     if rank == 0:
-        want = evaluate(full, args.kind, pos)[:, :, : args.splines]
-        res["peer_bitwise"] = bool(torch.equal(got, want))
+        res["peer_bitwise"] = bitwise
 
     def timed(fn):
         fn()
@@ -89,10 +96,10 @@ def main():
         e1.synchronize()
         return e0.elapsed_time(e1) / args.reps
 
-    res["peer_ms"] = timed(lambda: pg.evaluate(mine, pos))
+    res["peer_ms"] = timed(lambda: pg.evaluate(mine, pos, form=form))
     if own_gpu:
         def nccl_path():
-            block = evaluate(mine, args.kind, pos)[:, :, : hi - lo]
+            block = evaluate(mine, args.kind, pos, form=form)[:, :, : hi - lo]
             return gather_orbital_blocks(block, part, root=0) if world > 1 else block
         out = nccl_path()
         if rank == 0:

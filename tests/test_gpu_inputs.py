@@ -31,6 +31,6 @@ def test_tile_autotuner():
     assert res.best_tile in res.scanned and len(res.throughputs) == 4
     assert res.best_throughput == max(res.throughputs)
     assert all(t > 0 for t in res.throughputs)
-    # k-power form: every candidate carries it (dense probe -> the line kernel reads it)
-    res_kp = tune_tile_size(dt.with_kpower(), "vgh", n_positions=2 * 24 ** 3, repeats=2)
+    # opt-in k-power form: every candidate carries it and is timed on it
+    res_kp = tune_tile_size(dt, "vgh", n_positions=2 * 24 ** 3, repeats=2, kpower=True)
     assert res_kp.scanned == (32, 64, 128, 256) and all(t > 0 for t in res_kp.throughputs)

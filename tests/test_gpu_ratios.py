@@ -96,3 +96,38 @@ def test_ratios_line_path(torch, monkeypatch, kind, dtype):
     monkeypatch.delenv("SPO_LINE")
     want = reference_ratios(torch, dt, kind, pos[ok.numpy()], coef[ok.cuda()])
     assert float((a[ok.cuda()] - want).abs().max() / want.abs().max()) < rtol
+
+
+@pytest.mark.parametrize("line", ["0", "1"])
+@pytest.mark.parametrize("kind", ["v", "vgl", "vgh"])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_ratios_against_oracle(torch, monkeypatch, kind, dtype, line):
+    """Anchored on the f64 oracle: want[p, s] = sum_n
+    oracle(p, s, n) * coef[p, n] in fp64.  Bound: the north-star per-element
+    bound carried through the contraction, tol * sum_n sum|w*c|(p, s, n) *
+    |coef[p, n]|, with tol doubled for the lane dots' own rounding (fp32
+    products summed within 128-orbital chunks, fp64 across chunks)."""
+    import oracle
+
+    grid = unit_cell_grid(16)
+    rng = np.random.default_rng(12)
+    if dtype == "f32":
+        dt = DeviceTable.random(grid, 512, seed=9)
+        tdt, tol = torch.float32, 2e-5
+    else:
+        dt = DeviceTable.normal_f64(grid, 256, seed=9)
+        tdt, tol = torch.float64, 2e-12
+    P = 3 * 16 ** 3  # dense: the line path when SPO_LINE=1
+    pos = rng.random((P, 3)) * 2.0 - 0.5
+    coef_np = rng.standard_normal((P, dt.n_splines))
+    coef = torch.from_numpy(coef_np).to("cuda", tdt)
+    monkeypatch.setenv("SPO_LINE", line)
+    got = evaluate_ratios(dt, kind, pos, coef).cpu().numpy()
+    monkeypatch.delenv("SPO_LINE")
+    sel = np.arange(0, P, 7)
+    ref, scale = oracle.eval_f64(kind, dt.reference_soa(), dt.n_splines, grid.spacings, pos[sel])
+    c = coef.double().cpu().numpy()[sel]  # the coefficients as the kernel saw them
+    want = np.einsum("psn,pn->ps", ref, c)
+    bound = tol * np.einsum("psn,pn->ps", scale, np.abs(c))
+    err = np.abs(got[sel] - want)
+    assert (err <= bound).all(), float((err / bound).max())

@@ -1,5 +1,5 @@
 """Host-side mirror of the reference API (no GPU): grid spec, tables, fills,
-tiling, file format, output buffers, argument validation that happens before
+tiling, output buffers, argument validation that happens before
 any device call.  Mirrors pkg/tests/test_grid.py / test_coeffs.py."""
 import numpy as np
 import pytest
@@ -19,12 +19,9 @@ from paper_1611_02665_b200 import (
     build_table,
     collect_streams,
     convert_aos_to_soa,
-    dump_table,
     eval_batch,
     eval_tiled,
     eval_v,
-    load_table,
-    memory_footprint,
     padded_count,
     tile_table,
 )
@@ -91,7 +88,7 @@ def test_tiling_conserves_elements():
     tiled = tile_table(soa, 8)
     cat = np.concatenate([t.data[..., :8] for t in tiled.tiles], axis=-1)
     np.testing.assert_array_equal(cat, soa.data[..., :24])
-    assert memory_footprint(tiled) == 3 * 6 ** 3 * 16 * 4
+    assert tiled.nbytes == 3 * 6 ** 3 * 16 * 4
 
 
 def test_footprint_known_answer():
@@ -107,21 +104,6 @@ def test_tables_are_immutable():
         CoeffTableSoA(GridSpec(4, 4, 4), 3, np.zeros((4, 4, 4, 3), np.float32))
     with pytest.raises(ContractError):
         CoeffTableAoS(GridSpec(4, 4, 4), np.zeros((2, 4, 4, 5), np.float32))
-
-
-def test_dump_load_round_trip(tmp_path):
-    soa = build_table(GridSpec(4, 5, 6), 20, FillSpec.random(9))
-    path = tmp_path / "t.bspc"
-    dump_table(soa, path)
-    raw = path.read_bytes()
-    assert raw[:4] == b"BSPC"
-    assert list(np.frombuffer(raw[4:28], dtype="<u4")) == [1, 4, 5, 6, 20, 32]
-    back = load_table(path, spacings=(0.5, 0.5, 0.5))
-    np.testing.assert_array_equal(back.data, soa.data)
-    assert back.grid.dx == 0.5
-    path.write_bytes(b"XXXX" + raw[4:])
-    with pytest.raises(ContractError):
-        load_table(path)
 
 
 def test_output_buffers():
