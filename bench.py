@@ -404,7 +404,7 @@ def run_reference(args):
 
 # ----------------------------------------------------- configs 1-4 (fp32) --
 
-KERNELS_PER_CALL = {"line": 4, "tma": 3, "generic": 1}  # this repo's kernels per evaluate() (cub's sort not counted)
+KERNELS_PER_CALL = {"line": 4, "window": 4, "tma": 3, "generic": 1}  # this repo's kernels per evaluate() (cub's sort not counted)
 
 
 def kernel_label(path, kind, mode, form, dtype="float"):
@@ -412,6 +412,9 @@ def kernel_label(path, kind, mode, form, dtype="float"):
     return {
         "line": f"spo::line::line_kernel<{kind.upper()},{dtype},RATIO=false,KP={kp}> (+ line_keys, cub sort, "
                 f"line_records, line_runs prologue, timed together)",
+        "window": f"spo::line::line_kernel<{kind.upper()},{dtype},RATIO=false,KP=false,VGROUP=1,WIN=2> (window "
+                  f"variant: 5x5-row planes shared by 2x2 cells; + line_keys, cub sort, line_records, line_runs "
+                  f"prologue, timed together)",
         "tma": f"spo::tma::eval_tma_kernel<{kind.upper()},KP={kp}> (+ bucket_count, prologue_records, "
                f"timed together)",
         "generic": f"spo::eval_kernel<{kind.upper()},{dtype},{mode},KP={kp}>",

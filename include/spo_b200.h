@@ -160,11 +160,15 @@ int spo_eval_lanes(int kind, int dtype, int mode, const void *table, const int32
  *   SPO_PATH_LINE     line-window kernel: planes shared along grid lines, for
  *                     VGL/VGH batches of >= 1 position per grid cell, V of >= 2
  *                     (spo_eval_line.cu)
+ *   SPO_PATH_WINDOW   its window variant for sparse batches: (3+3) x (3+3)-row
+ *                     planes shared by the positions of 3 x 3 (j0, k0) cells
+ *                     (B-spline table form)
  * -1 on bad arguments.  All paths give bitwise identical results.
  */
 #define SPO_PATH_GENERIC 0
 #define SPO_PATH_TMA 1
 #define SPO_PATH_LINE 2
+#define SPO_PATH_WINDOW 3
 int spo_eval_path(int kind, int dtype, int mode, const int32_t *n3, int32_t nb, int32_t n_tiles, int64_t n_pos,
                   int64_t workspace_bytes);
 

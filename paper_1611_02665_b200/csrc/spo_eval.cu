@@ -334,7 +334,8 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
               long long n_pos, void *out, long long ops, long long oss, const long long *out_index, int *status,
               void *workspace, long long ws_bytes, cudaStream_t st, long long lane_limit,
               const void *coef = nullptr, long long coef_stride = 0, double *ratios = nullptr,
-              long long ratio_bytes = 0);
+              long long ratio_bytes = 0, int win = 1);
+int line_window_cells();
 long long eval_tma_ratio_bytes(int kind, int dtype, long long nb, long long n_tiles, long long n_pos);
 }
 
@@ -352,19 +353,30 @@ extern "C" int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64
     return a > b ? a : b;
 }
 
-// positions per grid cell from which the line-window kernel is used:
-// sustained-rate crossovers measured by scripts/micro/line_sustained.py and
-// scripts/bench_configs.py (V has little math per plane, so it needs more
-// sharing before the protocol pays: +15% at 2 positions per cell, -5% at 1)
-constexpr long long LINE_MIN_PER_CELL_VGX = 1, LINE_MIN_PER_CELL_V = 2;
+// Shared-plane kernels by density (positions per grid cell; sustained
+// interleaved timings, scripts/micro/window_ab.py, profiles/r02/window_ab.md):
+// the per-position TMA kernel below WINDOW_MIN_*; the window variant of the
+// line kernel ((2+3) x (2+3)-row planes shared by the positions of 2 x 2
+// (j0, k0) cells: +4% at 0.3/cell, +15-20% at 0.5-1/cell over the
+// per-position kernel, +1-5% over the line kernel up to 2.4/cell); the line
+// kernel from LINE_MIN_* (many positions per line: its V position groups
+// and fewer plane loads per slot pay).  k-power tables: no window variant
+// (rows have no z halo), the line kernel from 1 (VGL/VGH) / 2 (V) per cell.
+constexpr double WINDOW_MIN_VGX = 0.3, WINDOW_MIN_V = 0.4;
+constexpr double LINE_MIN_VGX = 4.0, LINE_MIN_V = 3.0;
+constexpr double KP_LINE_MIN_VGX = 1.0, KP_LINE_MIN_V = 2.0;
 
-// line-window kernel for batches dense enough to share stencil planes along
-// grid lines (SPO_LINE=0/1 forces it off/on; read on every call)
-static bool want_line(int kind, const int32_t *n3, long long n_pos) {
+// Which shared-plane kernel a FAST request takes: 0 = none (the per-position
+// TMA kernel), 1 = the line kernel, 3 = its window variant.  SPO_LINE=0/1/2
+// forces none / line / window (read on every call).
+static int line_variant(int kind, const int32_t *n3, long long n_pos, bool kpower) {
     const char *env_line = getenv("SPO_LINE");
-    if (env_line) return env_line[0] == '1';
-    const long long cells = (long long)n3[0] * n3[1] * n3[2];
-    return n_pos >= cells * (kind == SPO_KIND_V ? LINE_MIN_PER_CELL_V : LINE_MIN_PER_CELL_VGX);
+    if (env_line) return env_line[0] == '1' ? 1 : (env_line[0] == '2' && !kpower ? 3 : 0);
+    const double dens = (double)n_pos / ((double)n3[0] * n3[1] * n3[2]);
+    const bool v = kind == SPO_KIND_V;
+    if (kpower) return dens >= (v ? KP_LINE_MIN_V : KP_LINE_MIN_VGX) ? 1 : 0;
+    if (dens >= (v ? LINE_MIN_V : LINE_MIN_VGX)) return 1;
+    return dens >= (v ? WINDOW_MIN_V : WINDOW_MIN_VGX) ? 3 : 0;
 }
 
 // lane_limit < 0: every table lane is stored and `out` must be memory of the
@@ -430,10 +442,12 @@ static int eval_impl(int kind, int dtype, int mode, const void *table, const int
                 g.delta[ax] = delta3[ax];
                 g.n[ax] = n3[ax];
             }
-            if (want_line(kind, n3, n_pos)) {
+            const int lv = line_variant(kind, n3, n_pos, kpower);
+            if (lv) {
                 const int r = eval_line(kind, dtype, table, geo, g, pos, n_pos, out, out_pos_stride,
                                         out_stream_stride, reinterpret_cast<const long long *>(out_index), status,
-                                        workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream), lanes);
+                                        workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream), lanes,
+                                        nullptr, 0, nullptr, 0, lv == 3 ? line_window_cells() : 1);
                 if (r >= 0) return r;
             }
             const int r = eval_tma(kind, dtype, table, geo, g, pos, n_pos, out, out_pos_stride, out_stream_stride,
@@ -538,7 +552,8 @@ extern "C" int spo_eval_path(int kind, int dtype, int mode, const int32_t *n3, i
     if (mode != SPO_MODE_FAST || workspace_bytes <= 0) return SPO_PATH_GENERIC;
     const char *env_tma = getenv("SPO_TMA");
     if (env_tma && env_tma[0] == '0') return SPO_PATH_GENERIC;
-    if (want_line(kind, n3, n_pos) && eval_line_eligible(dtype, geo, n_pos, workspace_bytes)) return SPO_PATH_LINE;
+    const int lv = line_variant(kind, n3, n_pos, kpower);
+    if (lv && eval_line_eligible(dtype, geo, n_pos, workspace_bytes)) return lv == 3 ? SPO_PATH_WINDOW : SPO_PATH_LINE;
     if (workspace_bytes >= eval_tma_workspace_bytes(dtype, n_pos) && n_pos < (1LL << 31)) return SPO_PATH_TMA;
     return SPO_PATH_GENERIC;
 }

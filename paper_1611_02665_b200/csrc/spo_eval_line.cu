@@ -48,7 +48,6 @@ constexpr int ROWB = 512;                        // unit bytes per table row
 constexpr int BOXB = 512;                        // TMA box width in bytes
 static_assert(ROWB == BOXB, "one TMA box per plane");
 constexpr int BOX = 16 * BOXB;                   // bytes per box (16 rows)
-constexpr int PLANE = 16 * ROWB;                 // bytes per plane slot
 #ifndef SPO_LINE_BPL
 #define SPO_LINE_BPL 64
 #endif
@@ -153,7 +152,7 @@ struct LItem {
 
 // ------------------------------------------------------------- prologue --
 __global__ void line_keys_kernel(GridArgs g, const double *__restrict__ pos, long long n, unsigned *__restrict__ keys,
-                                 int *__restrict__ vals, int *__restrict__ status, int3 nbk) {
+                                 int *__restrict__ vals, int *__restrict__ status, int3 nbk, int win) {
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
          p += (long long)gridDim.x * blockDim.x) {
         double t;
@@ -163,8 +162,13 @@ __global__ void line_keys_kernel(GridArgs g, const double *__restrict__ pos, lon
         const int k0 = map_axis(z, g.dinv[2], g.cnt[2], &t);
         unsigned key = 0xffffffffu;
         if (isfinite(x) && isfinite(y) && isfinite(z)) {
-            const unsigned b = ((i0 * nbk.x / g.n[0]) * nbk.y + j0 * nbk.y / g.n[1]) * nbk.z + k0 * nbk.z / g.n[2];
-            key = (b << 24) | ((unsigned)j0 << 16) | ((unsigned)k0 << 8) | (unsigned)i0;
+            if (win > 1) {  // windows: all lines of a WIN x WIN window of (j0, k0) cells, in i0 order
+                key = ((unsigned)(j0 / win) << 16) | ((unsigned)(k0 / win) << 8) | (unsigned)i0;
+            } else {
+                const unsigned b =
+                    ((i0 * nbk.x / g.n[0]) * nbk.y + j0 * nbk.y / g.n[1]) * nbk.z + k0 * nbk.z / g.n[2];
+                key = (b << 24) | ((unsigned)j0 << 16) | ((unsigned)k0 << 8) | (unsigned)i0;
+            }
         } else if (status) {
             atomicOr(status, 1);
         }
@@ -211,8 +215,12 @@ __global__ void line_records_kernel(GridArgs g, const double *__restrict__ pos, 
 // run's first record the run's plane count; the producer loads planes in
 // that order and the consumers find their planes by number: plane number s
 // lives in ring slot s % R, phase s / R.
+// Windows (win > 1): a plane is the (win+3) x (win+3) rows at one i shared by
+// every position of a win x win window of (j0, k0) cells, anchored at the
+// window's first cell (plane entry: i | J << 10 | K << 20, J = win * (j0 / win));
+// positions of one window follow each other in i0 order like a line's.
 template <typename T>
-__global__ void line_runs_kernel(long long n, unsigned char *__restrict__ recs, int *__restrict__ plist) {
+__global__ void line_runs_kernel(long long n, unsigned char *__restrict__ recs, int *__restrict__ plist, int win) {
     constexpr int RECB = LT<T>::RECB;
     const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (b * BPL >= n) return;
@@ -226,7 +234,8 @@ __global__ void line_runs_kernel(long long n, unsigned char *__restrict__ recs, 
         int s = 0;
         if (cell.x >= 0) {
             const int j0 = cell.y & 0xffff, k0 = cell.y >> 16, i0 = cell.x;
-            const bool same = j0 == cj && k0 == ck;
+            const int wj = win * (j0 / win), wk = win * (k0 / win);  // the line's / window's anchor
+            const bool same = wj == cj && wk == ck;
             int lo;
             if (same && i0 <= last) {
                 s = next - 1 - (last - i0);
@@ -236,10 +245,10 @@ __global__ void line_runs_kernel(long long n, unsigned char *__restrict__ recs, 
                 lo = i0;
             }
             int *pl = plist + b * PL + 1;
-            for (int t = lo; t <= i0 + 3; ++t) pl[next++] = t | (j0 << 10) | (k0 << 20);
+            for (int t = lo; t <= i0 + 3; ++t) pl[next++] = t | (wj << 10) | (wk << 20);
             if (!same || i0 + 3 > last) last = i0 + 3;
-            cj = j0;
-            ck = k0;
+            cj = wj;
+            ck = wk;
         }
         c->z = s;
     }
@@ -247,24 +256,48 @@ __global__ void line_runs_kernel(long long n, unsigned char *__restrict__ recs, 
     plist[b * PL] = next;
 }
 
+// Plane slots: WIN = 1 (lines) R = LT<T>::R slots of 16 rows; windows of
+// WIN x WIN cells: as many (WIN+3)^2-row slots as the budget holds.
+constexpr size_t SMEM_BUDGET = 232448;
+template <int WIN>
+constexpr int plane_bytes() {
+    return (WIN + 3) * (WIN + 3) * ROWB;
+}
 template <typename T>
+constexpr size_t smem_fixed() {
+    return 2 * (size_t)BPL * LT<T>::RECB + 2 * (size_t)PLB + 2 * sizeof(LItem) + 4 * 8;
+}
+template <typename T, int WIN>
+constexpr int ring() {
+    return WIN == 1 ? LT<T>::R : (int)((SMEM_BUDGET - smem_fixed<T>()) / (plane_bytes<WIN>() + 16));
+}
+template <typename T, int WIN = 1>
 constexpr size_t smem_planes() {
-    return (size_t)LT<T>::R * PLANE;
+    return (size_t)ring<T, WIN>() * plane_bytes<WIN>();
 }
-template <typename T>
+template <typename T, int WIN = 1>
 constexpr size_t smem_bytes() {
-    return smem_planes<T>() + 2 * (size_t)BPL * LT<T>::RECB + 2 * (size_t)PLB + 2 * sizeof(LItem) +
-           (2 * LT<T>::R + 4) * 8;
+    return smem_planes<T, WIN>() + smem_fixed<T>() + 2 * (size_t)ring<T, WIN>() * 8;
 }
-static_assert(smem_bytes<float>() <= 232448, "shared memory budget");
-static_assert(smem_bytes<double>() <= 232448, "shared memory budget");
+#ifndef SPO_WIN_CELLS
+#define SPO_WIN_CELLS 2  // 2 and 3 within ~1-4% of each other, 2 ahead on most configs; 4 slower
+#endif
+constexpr int WIN_CELLS = SPO_WIN_CELLS;  // window side (cells) of the window variant
+static_assert(smem_bytes<float>() <= SMEM_BUDGET, "shared memory budget");
+static_assert(smem_bytes<double>() <= SMEM_BUDGET, "shared memory budget");
+static_assert(smem_bytes<float, WIN_CELLS>() <= SMEM_BUDGET, "shared memory budget");
+static_assert(smem_bytes<double, WIN_CELLS>() <= SMEM_BUDGET, "shared memory budget");
+static_assert(ring<double, WIN_CELLS>() >= 6, "a window ring must hold more than one position's planes");
 
 // ---------------------------------------------------------------- kernel --
-template <int KIND, typename T, bool RATIO, bool KP, int VGROUP = 1>
+template <int KIND, typename T, bool RATIO, bool KP, int VGROUP = 1, int WIN = 1>
 __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_constant__ CUtensorMap tmap, const LArgs a) {
     constexpr int S = NS<KIND>::S;
     constexpr int CONSUMERS = cons_warps<T, KP>();
-    constexpr int R = LT<T>::R;
+    constexpr int R = ring<T, WIN>();
+    constexpr int PB = plane_bytes<WIN>();         // bytes per plane slot
+    constexpr int RJ = WIN + 3;                    // k-rows per j-row of a slot
+    static_assert(WIN == 1 || (!KP && VGROUP == 1), "windows: B-spline form, one position per warp");
     constexpr int W = 16 / (int)sizeof(T);         // lanes per thread (16-byte vector)
     constexpr int RECB = LT<T>::RECB;
     constexpr int ULANES = ROWB / (int)sizeof(T);  // lanes per unit
@@ -275,7 +308,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
 
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char *planes = smem;
-    unsigned char *recs = smem + smem_planes<T>();
+    unsigned char *recs = smem + smem_planes<T, WIN>();
     int *plists = reinterpret_cast<int *>(recs + 2 * BPL * RECB);
     LItem *info = reinterpret_cast<LItem *>(plists + 2 * PL);
     unsigned long long *full = reinterpret_cast<unsigned long long *>(info + 2);
@@ -382,8 +415,8 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                     // every plane in order, so the parity cannot alias)
                     if (n > 0) mbar_wait(&full[sl], (n - 1) & 1);
                     const int c = pl[1 + t];
-                    mbar_arrive_expect_tx(&full[sl], PLANE);
-                    tma_load_5d(planes + (size_t)sl * PLANE, &tmap, &full[sl], lt, a.kmul * ((c >> 20) & 0x3ff),
+                    mbar_arrive_expect_tx(&full[sl], PB);
+                    tma_load_5d(planes + (size_t)sl * PB, &tmap, &full[sl], lt, a.kmul * ((c >> 20) & 0x3ff),
                                 (c >> 10) & 0x3ff, c & 0x3ff, tile, policy);
                 }
                 __syncwarp();
@@ -413,7 +446,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
         __syncwarp();
         if (lane == 0) st_release_shared(&relw[g], v);
     };
-    if constexpr (KIND == SPO_KIND_V && !RATIO && VGROUP > 1) {
+    if constexpr (KIND == SPO_KIND_V && !RATIO && VGROUP > 1 && WIN == 1) {
         // V: groups of VGROUP consecutive sorted positions, group k of a run
         // to warp k mod CONSUMERS.  V has little math per plane, so a plane's
         // shared-memory read is most of its cost: the group reads each plane
@@ -478,7 +511,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                     while (ld_acquire_shared(issued) <= x) __nanosleep(SPIN_NS);
                     const int sl = (int)(x % R);
                     mbar_wait(&full[sl], (x / R) & 1);
-                    const T *p = reinterpret_cast<const T *>(planes + (size_t)sl * PLANE) + lane * W;
+                    const T *p = reinterpret_cast<const T *>(planes + (size_t)sl * PB) + lane * W;
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         RV c[4];
@@ -569,6 +602,8 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                 continue;
             }
             const unsigned s0 = base + (unsigned)(cell.z & 0xffff);
+            // the position's 4 x 4 rows inside its slot (windows: offset by its cell in the window)
+            const int corner = WIN == 1 ? 0 : (((cell.y & 0xffff) % WIN) * RJ + (cell.y >> 16) % WIN) * BOXL;
             T wx[12], wy[12], wz[12];  // k-power tables: wz[0] = t_z, the rest unused
             load_weights(rec, wx, wy, wz);
 #pragma unroll
@@ -577,13 +612,13 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                 while (ld_acquire_shared(issued) <= x) __nanosleep(SPIN_NS);
                 const int sl = (int)(x % R);
                 mbar_wait(&full[sl], (x / R) & 1);
-                const T *p = reinterpret_cast<const T *>(planes + (size_t)sl * PLANE) + lane * W;
+                const T *p = reinterpret_cast<const T *>(planes + (size_t)sl * PB) + corner + lane * W;
                 if constexpr (KP) {
                     const T dz = (T)a.dz, dz2 = (T)a.dz2;
                     slab_contract_kp<KIND, BOXL>(p, wy, wz[0], wx[i], wx[4 + i], wx[8 + i], mul_rn(wx[i], dz),
                                                  mul_rn(wx[4 + i], dz), mul_rn(wx[i], dz2), acc);
                 } else {
-                    slab_contract<KIND, BOXL>(p, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
+                    slab_contract<KIND, BOXL, RJ>(p, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
                 }
             }
             qn = a.dynamic ? take() : q + CONSUMERS;
@@ -611,18 +646,21 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
     }
 }
 
-template <int KIND, typename T, bool RATIO, bool KP, int VGROUP = 1>
+template <int KIND, typename T, bool RATIO, bool KP, int VGROUP = 1, int WIN = 1>
 static int launch1(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
-    constexpr size_t sm = smem_bytes<T>();
+    constexpr size_t sm = smem_bytes<T, WIN>();
     int grid = (int)min((long long)sms, a.n_items);
     if (grid < 1) grid = 1;
-    cudaFuncSetAttribute(line_kernel<KIND, T, RATIO, KP, VGROUP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(line_kernel<KIND, T, RATIO, KP, VGROUP, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
-    line_kernel<KIND, T, RATIO, KP, VGROUP><<<grid, threads<T, KP>(), sm, st>>>(map, a);
+    line_kernel<KIND, T, RATIO, KP, VGROUP, WIN><<<grid, threads<T, KP>(), sm, st>>>(map, a);
     return check_launch("spo_eval (line) launch");
 }
 template <int KIND, typename T, bool RATIO, bool KP>
-static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
+static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st, int win) {
+    if constexpr (!KP) {
+        if (win > 1) return launch1<KIND, T, RATIO, false, 1, WIN_CELLS>(map, a, sms, st);
+    }
     if constexpr (KIND == SPO_KIND_V && !RATIO) {
         // V positions per consumer warp by density (scripts/micro/vm_sweep.py,
         // profiles/r01/v_groups.jsonl): fp32 2 below 3.5 positions per cell,
@@ -641,9 +679,11 @@ static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t 
     return launch1<KIND, T, RATIO, KP>(map, a, sms, st);
 }
 template <int KIND, typename T>
-static int launch_r(bool ratio, bool kp, const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
-    if (kp) return ratio ? launch<KIND, T, true, true>(map, a, sms, st) : launch<KIND, T, false, true>(map, a, sms, st);
-    return ratio ? launch<KIND, T, true, false>(map, a, sms, st) : launch<KIND, T, false, false>(map, a, sms, st);
+static int launch_r(bool ratio, bool kp, const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st, int win) {
+    if (kp)
+        return ratio ? launch<KIND, T, true, true>(map, a, sms, st, 1) : launch<KIND, T, false, true>(map, a, sms, st, 1);
+    return ratio ? launch<KIND, T, true, false>(map, a, sms, st, win)
+                 : launch<KIND, T, false, false>(map, a, sms, st, win);
 }
 
 static size_t pad256(size_t b) { return (b + 255) / 256 * 256; }
@@ -687,6 +727,8 @@ bool eval_line_eligible(int dtype, const TableGeom &geo, long long n_pos, long l
     return ws_bytes >= eval_line_workspace_bytes(dtype, n_pos);
 }
 
+int line_window_cells() { return line::WIN_CELLS; }
+
 // Returns -1 when the request is not taken (the caller falls back).
 int ratio_reduce(int kind, const double *partials, long long units, long long n_pos, double *ratios,
                  cudaStream_t st);
@@ -694,10 +736,11 @@ int ratio_reduce(int kind, const double *partials, long long units, long long n_
 int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, const GridArgs &g, const double *pos,
               long long n_pos, void *out, long long ops, long long oss, const long long *out_index, int *status,
               void *workspace, long long ws_bytes, cudaStream_t st, long long lane_limit, const void *coef,
-              long long coef_stride, double *ratios, long long ratio_bytes) {
+              long long coef_stride, double *ratios, long long ratio_bytes, int win) {
     using namespace line;
     const bool ratio = ratios != nullptr;
     if (!eval_line_eligible(dtype, geo, n_pos, ws_bytes - ratio_bytes) || !aligned16(workspace)) return -1;
+    if (win != 1 && (win != WIN_CELLS || geo.kmul != 1)) return -1;  // windows: the B-spline form
     if (!tensor_map_encoder()) return -1;
     const int E = dtype == SPO_F64 ? 8 : 4;
     const int boxl = BOXB / E;
@@ -722,7 +765,7 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     int *plist = reinterpret_cast<int *>(recs + pad256((size_t)n_pos * (dtype == SPO_F64 ? LT<double>::RECB
                                                                                           : LT<float>::RECB)));
     CUtensorMap map;
-    const int r = table_tensor_map(&map, table, geo, dtype, boxl);
+    const int r = table_tensor_map(&map, table, geo, dtype, boxl, win + 3);
     if (r) return fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", r);
 
     if (cudaMemsetAsync(ws, 0, WS_HEADER, st) != cudaSuccess) return check_launch("workspace reset");
@@ -734,17 +777,17 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
         sscanf(e, "%d,%d,%d", &nbk.x, &nbk.y, &nbk.z);
         if (nbk.x * nbk.y * nbk.z > 255) nbk = make_int3(NBK, NBK, NBK);
     }
-    line_keys_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, keys_in, vals_in, status, nbk);
+    line_keys_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, keys_in, vals_in, status, nbk, win);
     if (cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, vals, (int)n_pos, 0, 32, st) != cudaSuccess)
         return check_launch("spo_eval (line sort)");
     const int *order = vals.Current();  // the sorted original indices (either buffer)
     const unsigned run_blocks = (unsigned)((n_pos + (long long)BPL * 128 - 1) / ((long long)BPL * 128));
     if (dtype == SPO_F64) {
         line_records_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(g, pos, order, n_pos, recs, geo.kmul != 1);
-        line_runs_kernel<double><<<run_blocks, 128, 0, st>>>(n_pos, recs, plist);
+        line_runs_kernel<double><<<run_blocks, 128, 0, st>>>(n_pos, recs, plist, win);
     } else {
         line_records_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(g, pos, order, n_pos, recs, geo.kmul != 1);
-        line_runs_kernel<float><<<run_blocks, 128, 0, st>>>(n_pos, recs, plist);
+        line_runs_kernel<float><<<run_blocks, 128, 0, st>>>(n_pos, recs, plist, win);
     }
     int rc = check_launch("spo_eval (line prologue)");
     if (rc) return rc;
@@ -785,13 +828,13 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (dtype == SPO_F64)
-        rc = kind == SPO_KIND_V     ? launch_r<SPO_KIND_V, double>(ratio, kp, map, a, sms, st)
-             : kind == SPO_KIND_VGL ? launch_r<SPO_KIND_VGL, double>(ratio, kp, map, a, sms, st)
-                                    : launch_r<SPO_KIND_VGH, double>(ratio, kp, map, a, sms, st);
+        rc = kind == SPO_KIND_V     ? launch_r<SPO_KIND_V, double>(ratio, kp, map, a, sms, st, win)
+             : kind == SPO_KIND_VGL ? launch_r<SPO_KIND_VGL, double>(ratio, kp, map, a, sms, st, win)
+                                    : launch_r<SPO_KIND_VGH, double>(ratio, kp, map, a, sms, st, win);
     else
-        rc = kind == SPO_KIND_V     ? launch_r<SPO_KIND_V, float>(ratio, kp, map, a, sms, st)
-             : kind == SPO_KIND_VGL ? launch_r<SPO_KIND_VGL, float>(ratio, kp, map, a, sms, st)
-                                    : launch_r<SPO_KIND_VGH, float>(ratio, kp, map, a, sms, st);
+        rc = kind == SPO_KIND_V     ? launch_r<SPO_KIND_V, float>(ratio, kp, map, a, sms, st, win)
+             : kind == SPO_KIND_VGL ? launch_r<SPO_KIND_VGL, float>(ratio, kp, map, a, sms, st, win)
+                                    : launch_r<SPO_KIND_VGH, float>(ratio, kp, map, a, sms, st, win);
     if (rc || !ratio) return rc;
     return ratio_reduce(kind, a.partials, units, n_pos, ratios, st);
 }

@@ -28,7 +28,10 @@ inline EncodeTiledFn tensor_map_encoder() {
     return fn;
 }
 
-inline int table_tensor_map(CUtensorMap *map, const void *table, const TableGeom &geo, int dtype, int box_lanes) {
+// box: box_lanes lanes x box_rows k-rows x box_rows j-rows of one i-plane
+// (4 x 4: one position's slab; larger: a window of several positions' slabs)
+inline int table_tensor_map(CUtensorMap *map, const void *table, const TableGeom &geo, int dtype, int box_lanes,
+                            int box_rows = 4) {
     EncodeTiledFn encode = tensor_map_encoder();
     if (!encode) return -1;
     const cuuint64_t E = dtype == SPO_F64 ? 8 : 4;
@@ -36,7 +39,7 @@ inline int table_tensor_map(CUtensorMap *map, const void *table, const TableGeom
                           (cuuint64_t)geo.n_tiles};
     cuuint64_t strides[4] = {(cuuint64_t)geo.nb * E, (cuuint64_t)geo.nzp * geo.nb * E,
                              (cuuint64_t)geo.nyp * geo.nzp * geo.nb * E, (cuuint64_t)geo.tile_stride * E};
-    cuuint32_t box[5] = {(cuuint32_t)box_lanes, 4, 4, 1, 1};
+    cuuint32_t box[5] = {(cuuint32_t)box_lanes, (cuuint32_t)box_rows, (cuuint32_t)box_rows, 1, 1};
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     const CUresult r =
         encode(map, dtype == SPO_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5,
@@ -146,8 +149,10 @@ __device__ __forceinline__ float2 fma2(float w, float2 c, float2 acc) {
 __device__ __forceinline__ float2 mul2(float w, float2 c) { return __fmul2_rn(make_float2(w, w), c); }
 
 // One i-slab for one lane: 4 fp32 orbitals as two fp32x2 pairs.
-// slab: [j][k][CW] of this lane's position; wy/wz: 12 weights; ax/dax/d2ax: x weights of this i.
-template <int KIND, int CW>
+// slab: [j][k][CW] of this lane's position, RJ k-rows per j (4: a slab of its
+// own; more: the position's 4 x 4 corner of a window of rows); wy/wz: 12
+// weights; ax/dax/d2ax: x weights of this i.
+template <int KIND, int CW, int RJ = 4>
 __device__ __forceinline__ void slab_contract(const float *__restrict__ slab, const float (&wy)[12],
                                               const float (&wz)[12], float ax, float dax, float d2ax,
                                               float2 (&acc)[NS<KIND>::S][2]) {
@@ -158,7 +163,7 @@ __device__ __forceinline__ void slab_contract(const float *__restrict__ slab, co
     for (int j = 0; j < 4; ++j) {
         float4 c[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const float4 *>(slab + (j * 4 + k) * CW);
+        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const float4 *>(slab + (j * RJ + k) * CW);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const float2 c0 = h ? make_float2(c[0].z, c[0].w) : make_float2(c[0].x, c[0].y);
@@ -199,7 +204,7 @@ __device__ __forceinline__ void slab_contract(const float *__restrict__ slab, co
 }
 
 // One i-slab for one lane: 2 fp64 orbitals, DFMA in the generic kernel's order.
-template <int KIND, int CW>
+template <int KIND, int CW, int RJ = 4>
 __device__ __forceinline__ void slab_contract(const double *__restrict__ slab, const double (&wy)[12],
                                               const double (&wz)[12], double ax, double dax, double d2ax,
                                               double2 (&acc)[NS<KIND>::S][1]) {
@@ -210,7 +215,7 @@ __device__ __forceinline__ void slab_contract(const double *__restrict__ slab, c
     for (int j = 0; j < 4; ++j) {
         double2 c[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const double2 *>(slab + (j * 4 + k) * CW);
+        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const double2 *>(slab + (j * RJ + k) * CW);
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             const double c0 = e ? c[0].y : c[0].x, c1 = e ? c[1].y : c[1].x;

@@ -323,14 +323,16 @@ def evaluate(table, kind, positions, out=None, *, mode: str = "fast", out_index=
     return out
 
 
-_PATHS = {0: "generic", 1: "tma", 2: "line"}
+_PATHS = {0: "generic", 1: "tma", 2: "line", 3: "window"}
 
 
 def eval_path(table, kind, n_positions: int, *, mode: str = "fast", pipeline="auto", form: str = "auto") -> str:
     """The kernel evaluate() runs for this request: "generic" (one pass),
-    "tma" (per-position TMA pipeline) or "line" (planes shared along grid
-    lines) -- spo_eval_path; all give bitwise identical results on the same
-    table form (eval_form() tells which form)."""
+    "tma" (per-position TMA pipeline), "line" (planes shared along grid
+    lines) or "window" (the line kernel's variant for sparser batches:
+    planes shared by the positions of 2 x 2 (j0, k0) cells) -- spo_eval_path;
+    all give bitwise identical results on the same table form (eval_form()
+    tells which form)."""
     kind = as_kind(kind)
     dt = as_device_table(table)
     L = _abi.load()

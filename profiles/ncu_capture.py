@@ -47,7 +47,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "KB
          "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
          "hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9, "cycle/second": 1, "cycle/nsecond": 1e9,
          "cycle/usecond": 1e6, "%": 1}
-KERNEL_RE = {"line": "line_kernel", "tma": "eval_tma_kernel", "generic": "eval_kernel"}
+KERNEL_RE = {"line": "line_kernel", "window": "line_kernel", "tma": "eval_tma_kernel", "generic": "eval_kernel"}
 
 
 def parse_raw(rep):

@@ -2,8 +2,9 @@
 """Randomised stress of the line-window kernel's synchronisation (plane ring,
 shared position counter, position groups): random grids, orbital counts,
 kinds, dtypes, table forms and densities, each evaluated by the line kernel
-(SPO_LINE=1) and the per-position TMA kernel (SPO_LINE=0) -- the results must
-be bitwise equal.  Exits non-zero on the first mismatch.
+(SPO_LINE=1), its window variant (SPO_LINE=2; k-power tables fall back to the
+per-position kernel) and the per-position TMA kernel (SPO_LINE=0) -- the
+results must be bitwise equal.  Exits non-zero on the first mismatch.
 
     python scripts/stress_line.py [iterations] [seed]
 """
@@ -38,25 +39,25 @@ def main():
         if form == "kpower":
             dt.with_kpower()
         kind = ["v", "vgl", "vgh"][int(rng.integers(0, 3))]
-        dens = float(rng.choice([0.3, 0.8, 1.5, 3.0, 6.0, 17.0]))
+        dens = float(rng.choice([0.05, 0.15, 0.3, 0.8, 1.5, 3.0, 6.0, 17.0]))
         P = max(1, int(dens * np.prod(n3))) + int(rng.integers(0, 64))
         pos = rng.random((P, 3)) * 3.0 - 1.0
         if rng.random() < 0.2:
             pos[rng.integers(0, P, size=3), rng.integers(0, 3, size=3)] = np.nan
         dpos = torch.from_numpy(pos).cuda()
         outs = []
-        for line in ("1", "0"):
+        for line in ("1", "2", "0"):
             os.environ["SPO_LINE"] = line
             st = torch.zeros(1, dtype=torch.int32, device="cuda")
             outs.append(evaluate(dt, kind, dpos, pipeline=True, form=form, status=st, check=False))
         torch.cuda.synchronize()
-        a, b = (o.nan_to_num(123.0) for o in outs)
-        ok = bool(torch.equal(a, b))
+        a, w, b = (o.nan_to_num(123.0) for o in outs)
+        ok = bool(torch.equal(a, b)) and bool(torch.equal(w, b))
         print(f"{it:3d} grid={n3} N={n} {'f64' if f64 else 'f32'} tile={tile} {form} {kind} P={P} "
               f"({dens}/cell) {'ok' if ok else 'MISMATCH'}", flush=True)
         if not ok:
             return 1
-        del dt, outs, a, b
+        del dt, outs, a, w, b
         torch.cuda.empty_cache()
     print(f"all {iters} cases bitwise equal ({time.time() - t0:.0f} s)")
     return 0

@@ -42,7 +42,7 @@ def test_b200_arm_contract():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
-    assert d["config"]["path"] in ("line", "tma", "generic")
+    assert d["config"]["path"] in ("line", "window", "tma", "generic")
 
 
 def _torchrun(args, port, timeout=900):

@@ -16,8 +16,8 @@ zeros of w3, da1, d2a2 and d2a1 (a zero weight has a zero scale: the output
 must then be exactly 0).
 
 The B-spline table form (the default, form="auto"/"bspline") meets the
-north-star bound on all of it, on all three kernels (generic, per-position
-TMA, line), fp32 and fp64.  The opt-in k-power form meets only its documented
+north-star bound on all of it, on every kernel (generic, per-position TMA,
+line, window), fp32 and fp64.  The opt-in k-power form meets only its documented
 weaker bound, tol * (sum|w*c| + oracle.kpower_scale), the second term being
 relative to the power-basis coefficient magnitudes -- and demonstrably NOT
 the north-star one, which is why form="auto" never picks it.
@@ -85,7 +85,7 @@ def case(request):
 
 def _paths(monkeypatch, dt, kind, pos, form):
     outs = {"generic": evaluate(dt, kind, pos, pipeline=False, form=form)}
-    for name, v in (("tma", "0"), ("line", "1")):
+    for name, v in (("tma", "0"), ("line", "1")) + ((("window", "2"),) if form != "kpower" else ()):
         monkeypatch.setenv("SPO_LINE", v)
         outs[name] = evaluate(dt, kind, pos, pipeline=True, form=form)
     monkeypatch.delenv("SPO_LINE")

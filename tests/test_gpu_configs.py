@@ -1,12 +1,12 @@
 """GPU parity on the BASELINE configs 2-5 at full size.
 
 Per config and kind, on BOTH table forms (the default B-spline form and the
-opt-in k-power form) and on ALL THREE fast kernel paths (generic, per-position
-TMA, line-window -- forced with SPO_LINE / pipeline so every path runs the
-same full launch):
+opt-in k-power form) and on EVERY fast kernel path (generic, per-position
+TMA, line, and the window variant of the line kernel on the B-spline form --
+forced with SPO_LINE / pipeline so every path runs the same full launch):
 
-* the three paths' full outputs are bitwise identical (per-position digests
-  of every output bit);
+* the paths' full outputs are bitwise identical (per-position digests of
+  every output bit);
 * >= 2048 oracle positions per (config, kind, form, path), stratified: one
   from every 4x4x4-cell block of the grid, the first and last position of
   line-kernel runs, random ones on top (tests/strata.py), each within
@@ -36,7 +36,7 @@ from strata import stratified_sample
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 TOL32, TOL64 = 1e-5, 1e-12
-PATHS = ("line", "tma", "generic")
+PATHS = ("line", "window", "tma", "generic")
 FORMS = ("bspline", "kpower")
 N_ORACLE = 2048
 N_STRICT = 16384
@@ -64,7 +64,7 @@ def run_path(monkeypatch, dt, kind, pos, out, path, form):
     if path == "generic":
         evaluate(dt, kind, pos, out, pipeline=False, form=form, check=False)
         return
-    monkeypatch.setenv("SPO_LINE", "1" if path == "line" else "0")
+    monkeypatch.setenv("SPO_LINE", {"line": "1", "window": "2", "tma": "0"}[path])
     try:
         assert eval_path(dt, kind, pos.shape[0], pipeline=True, form=form) == path
         evaluate(dt, kind, pos, out, pipeline=True, form=form, check=False)
@@ -109,6 +109,8 @@ def check_launches(torch, monkeypatch, dt, host, kind, pos, launch, tol, forms=F
     for form in forms:
         digests = {}
         for path in PATHS:
+            if path == "window" and form == "kpower":
+                continue  # the window variant reads the B-spline form only
             dg, got = [], np.empty((sel.size, S, dt.n_splines), dtype=dt.dtype)
             for lo in range(0, P, launch):
                 hi = min(P, lo + launch)
@@ -122,6 +124,8 @@ def check_launches(torch, monkeypatch, dt, host, kind, pos, launch, tol, forms=F
             assert ok, (kind, form, path, worst)
             report[(form, path)] = worst
         assert torch.equal(digests["line"], digests["tma"]), (kind, form)
+        if "window" in digests:
+            assert torch.equal(digests["window"], digests["tma"]), (kind, form)
         assert torch.equal(digests["line"], digests["generic"]), (kind, form)
     del out
     return report
@@ -195,7 +199,7 @@ def test_config4_full_workload(torch, monkeypatch):
     pos = config_positions(cfg)["vgh"]
     assert pos.shape == (1048576, 3)
     host = dt.reference_soa()
-    assert eval_path(dt, "vgh", 524288) == "line" and eval_form(dt, "vgh", 524288) == "bspline"
+    assert eval_path(dt, "vgh", 524288) == "window" and eval_form(dt, "vgh", 524288) == "bspline"
     check_launches(torch, monkeypatch, dt, host, "vgh", pos, 524288, TOL32, n_min=4096)
     check_strict(dt, host, "vgh", pos[:N_STRICT])
     del host

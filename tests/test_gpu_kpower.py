@@ -197,7 +197,8 @@ def test_kpower_auto_policy():
     dt = DeviceTable.random(unit_cell_grid(16), 256, seed=4).with_kpower()
     dense = np.random.default_rng(1).random((2 * 16 ** 3, 3))
     sparse = dense[:600]
-    assert eval_path(dt, "vgh", len(dense)) == "line"
+    assert eval_path(dt, "vgh", len(dense)) == "window"  # 2 per cell, B-spline form
+    assert eval_path(dt, "vgh", len(dense), form="kpower") == "line"
     for p in (dense, sparse):
         assert eval_form(dt, "vgh", len(p)) == "bspline"
         assert eval_form(dt, "vgh", len(p), form="kpower") == "kpower"

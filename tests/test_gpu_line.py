@@ -2,8 +2,9 @@
 lines) is bitwise identical to the per-position TMA kernel and the generic
 kernel on every input class: kinds, fp32/fp64, tiled/untiled tables, ragged
 runs, duplicate cells, a single line, non-finite positions, out_index,
-lane_limit, and grids too large for its sort key (fallback).  SPO_LINE=1/0
-forces the path (read on every call)."""
+lane_limit, and grids too large for its sort key (fallback) -- and so is its
+window variant for sparse batches.  SPO_LINE=1/2/0 forces the line kernel,
+the window variant or the per-position kernel (read on every call)."""
 import numpy as np
 import pytest
 
@@ -15,11 +16,15 @@ pytestmark = pytest.mark.gpu
 
 
 def _both(monkeypatch, dt, kind, pos, **kw):
+    """(line, per-position) outputs; the window variant must equal both."""
     monkeypatch.setenv("SPO_LINE", "1")
     a = evaluate(dt, kind, pos, pipeline=True, **kw).clone()
+    monkeypatch.setenv("SPO_LINE", "2")
+    w = evaluate(dt, kind, pos, pipeline=True, **kw).clone()
     monkeypatch.setenv("SPO_LINE", "0")
     b = evaluate(dt, kind, pos, pipeline=True, **kw)
     monkeypatch.delenv("SPO_LINE")
+    assert _eq(w, b), "window variant differs from the per-position kernel"
     return a, b
 
 
