@@ -114,6 +114,14 @@ __device__ __forceinline__ void contract_fast(const T *__restrict__ rp, long lon
     for (int s = 0; s < Streams<KIND>::S; ++s)
 #pragma unroll
         for (int e = 0; e < W; ++e) acc[s][e] = T(0);
+    // fp32 B-spline tables: the z second derivative through the (ax ay)-weighted
+    // z rows, as spo_tma.cuh slab_contract / finish_z2 (same sequence, bitwise)
+    constexpr bool Z2 = !KP && sizeof(T) == 4 && KIND != SPO_KIND_V;
+    T zs[4][W];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int e = 0; e < W; ++e) zs[c][e] = T(0);
 
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -129,6 +137,7 @@ __device__ __forceinline__ void contract_fast(const T *__restrict__ rp, long lon
             ld16(r + sk, c1);
             ld16(r + 2 * sk, c2);
             ld16(r + 3 * sk, c3);
+            const T axy = mulT(wx[i], wy[j]);
 #pragma unroll
             for (int e = 0; e < W; ++e) {
                 T s0, s1, s2;
@@ -145,7 +154,8 @@ __device__ __forceinline__ void contract_fast(const T *__restrict__ rp, long lon
                     s0 = fmaT(wz[3], c3[e], fmaT(wz[2], c2[e], fmaT(wz[1], c1[e], wz[0] * c0[e])));
                     if (KIND != SPO_KIND_V) {
                         s1 = fmaT(wz[7], c3[e], fmaT(wz[6], c2[e], fmaT(wz[5], c1[e], wz[4] * c0[e])));
-                        s2 = fmaT(wz[11], c3[e], fmaT(wz[10], c2[e], fmaT(wz[9], c1[e], wz[8] * c0[e])));
+                        if constexpr (!Z2)
+                            s2 = fmaT(wz[11], c3[e], fmaT(wz[10], c2[e], fmaT(wz[9], c1[e], wz[8] * c0[e])));
                     }
                 }
                 t00[e] = fmaT(wy[j], s0, t00[e]);
@@ -153,8 +163,15 @@ __device__ __forceinline__ void contract_fast(const T *__restrict__ rp, long lon
                     t10[e] = fmaT(wy[4 + j], s0, t10[e]);
                     t01[e] = fmaT(wy[j], s1, t01[e]);
                     t20[e] = fmaT(wy[8 + j], s0, t20[e]);
-                    t02[e] = fmaT(wy[j], s2, t02[e]);
                     if (KIND == SPO_KIND_VGH) t11[e] = fmaT(wy[4 + j], s1, t11[e]);
+                    if constexpr (Z2) {
+                        zs[0][e] = fmaT(axy, c0[e], zs[0][e]);
+                        zs[1][e] = fmaT(axy, c1[e], zs[1][e]);
+                        zs[2][e] = fmaT(axy, c2[e], zs[2][e]);
+                        zs[3][e] = fmaT(axy, c3[e], zs[3][e]);
+                    } else {
+                        t02[e] = fmaT(wy[j], s2, t02[e]);
+                    }
                 }
             }
         }
@@ -171,8 +188,11 @@ __device__ __forceinline__ void contract_fast(const T *__restrict__ rp, long lon
                 acc[3][e] = fmaT(axz, t01[e], acc[3][e]);        // gz
             }
             if (KIND == SPO_KIND_VGL) {
-                // l = d2x*t00 + x*t20 + x*t02
-                acc[4][e] = fmaT(wx[8 + i], t00[e], fmaT(wx[i], t20[e], fmaT(axz2, t02[e], acc[4][e])));
+                // l = d2x*t00 + x*t20 + x*t02 (Z2: the z term after the loop)
+                if constexpr (Z2)
+                    acc[4][e] = fmaT(wx[8 + i], t00[e], fmaT(wx[i], t20[e], acc[4][e]));
+                else
+                    acc[4][e] = fmaT(wx[8 + i], t00[e], fmaT(wx[i], t20[e], fmaT(axz2, t02[e], acc[4][e])));
             }
             if (KIND == SPO_KIND_VGH) {
                 acc[4][e] = fmaT(wx[8 + i], t00[e], acc[4][e]);  // hxx
@@ -180,8 +200,16 @@ __device__ __forceinline__ void contract_fast(const T *__restrict__ rp, long lon
                 acc[6][e] = fmaT(daxz, t01[e], acc[6][e]);       // hxz
                 acc[7][e] = fmaT(wx[i], t20[e], acc[7][e]);      // hyy
                 acc[8][e] = fmaT(axz, t11[e], acc[8][e]);        // hyz
-                acc[9][e] = fmaT(axz2, t02[e], acc[9][e]);       // hzz
+                if constexpr (!Z2) acc[9][e] = fmaT(axz2, t02[e], acc[9][e]);  // hzz
             }
+        }
+    }
+    if constexpr (Z2) {
+#pragma unroll
+        for (int e = 0; e < W; ++e) {
+            const T zz = fmaT(wz[11], zs[3][e], fmaT(wz[10], zs[2][e], fmaT(wz[9], zs[1][e], wz[8] * zs[0][e])));
+            if (KIND == SPO_KIND_VGH) acc[9][e] = zz;
+            if (KIND == SPO_KIND_VGL) acc[4][e] = addT(acc[4][e], zz);
         }
     }
 }

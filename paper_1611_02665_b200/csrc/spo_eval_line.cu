@@ -442,6 +442,15 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(LW<T, KP>::CREG));
     const int g = warp - 4;
     unsigned base = 0;
+    // `issued` only grows: a value once observed (acquire) covers every plane
+    // below it, so the poll is skipped for those (saves an acquire load per plane)
+    unsigned seen = 0;
+    auto await_issued = [&](unsigned x) {
+        if (x < seen) return;
+        unsigned v;
+        while ((v = ld_acquire_shared(issued)) <= x) __nanosleep(SPIN_NS);
+        seen = v;
+    };
     auto publish = [&](unsigned v) {
         __syncwarp();
         if (lane == 0) st_release_shared(&relw[g], v);
@@ -508,7 +517,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                     t00[m][0] = t00[m][1] = TV{};
                 }
                 for (unsigned x = lo; lo != 0xffffffffu && x <= hi; ++x) {
-                    while (ld_acquire_shared(issued) <= x) __nanosleep(SPIN_NS);
+                    await_issued(x);
                     const int sl = (int)(x % R);
                     mbar_wait(&full[sl], (x / R) & 1);
                     const T *p = reinterpret_cast<const T *>(planes + (size_t)sl * PB) + lane * W;
@@ -580,11 +589,15 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
             const int4 cell = *reinterpret_cast<const int4 *>(rec + 36 * sizeof(T));
             const long long op = a.out_index ? a.out_index[cell.w] : cell.w;
             T *o = reinterpret_cast<T *>(a.out) + op * a.out_pos_stride + L0;
-            AV acc[S][AN];
+            AV acc[S][AN], zs[4][AN];  // zs: fp32 z-second-derivative sums (slab_contract)
 #pragma unroll
             for (int s = 0; s < S; ++s)
 #pragma unroll
                 for (int h = 0; h < AN; ++h) zero(acc[s][h]);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int h = 0; h < AN; ++h) zero(zs[c][h]);
             if (cell.x < 0) {
                 qn = a.dynamic ? take() : q + CONSUMERS;
                 publish(first_plane(qn));
@@ -609,7 +622,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const unsigned x = s0 + (unsigned)i;
-                while (ld_acquire_shared(issued) <= x) __nanosleep(SPIN_NS);
+                await_issued(x);
                 const int sl = (int)(x % R);
                 mbar_wait(&full[sl], (x / R) & 1);
                 const T *p = reinterpret_cast<const T *>(planes + (size_t)sl * PB) + corner + lane * W;
@@ -617,10 +630,13 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                     const T dz = (T)a.dz, dz2 = (T)a.dz2;
                     slab_contract_kp<KIND, BOXL>(p, wy, wz[0], wx[i], wx[4 + i], wx[8 + i], mul_rn(wx[i], dz),
                                                  mul_rn(wx[4 + i], dz), mul_rn(wx[i], dz2), acc);
+                } else if constexpr (sizeof(T) == 4) {
+                    slab_contract<KIND, BOXL, RJ>(p, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc, zs);
                 } else {
                     slab_contract<KIND, BOXL, RJ>(p, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
                 }
             }
+            if constexpr (!KP && sizeof(T) == 4) finish_z2<KIND>(wz, zs, acc);
             qn = a.dynamic ? take() : q + CONSUMERS;
             publish(first_plane(qn));  // this position's planes are read
             if constexpr (RATIO) {

@@ -315,11 +315,15 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
             T wx[12], wy[12], wz[12];
             load_weights(rc + min(p, it.nb - 1) * RECB, wx, wy, wz);
             const int4 cell = *reinterpret_cast<const int4 *>(rc + min(p, it.nb - 1) * RECB + 36 * sizeof(T));
-            AV acc[S][AN];
+            AV acc[S][AN], zs[4][AN];  // zs: fp32 z-second-derivative sums (slab_contract)
 #pragma unroll
             for (int s = 0; s < S; ++s)
 #pragma unroll
                 for (int h = 0; h < AN; ++h) zero(acc[s][h]);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int h = 0; h < AN; ++h) zero(zs[c][h]);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 // ---- issue the next step into the other stage (its previous
@@ -359,11 +363,14 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
                     const T dz = (T)a.dz, dz2 = (T)a.dz2;
                     slab_contract_kp<KIND, CW>(slab, wy, wz[0], wx[i], wx[4 + i], wx[8 + i], mul_rn(wx[i], dz),
                                                mul_rn(wx[4 + i], dz), mul_rn(wx[i], dz2), acc);
+                } else if constexpr (sizeof(T) == 4) {
+                    slab_contract<KIND, CW>(slab, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc, zs);
                 } else {
                     slab_contract<KIND, CW>(slab, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
                 }
                 st ^= 1;
             }
+            if constexpr (!KP && sizeof(T) == 4) finish_z2<KIND>(wz, zs, acc);
             if constexpr (RATIO) {
                 const bool live = p < it.nb;
                 const long long gp = live ? cell.w : 0;

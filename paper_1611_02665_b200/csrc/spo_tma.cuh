@@ -152,18 +152,29 @@ __device__ __forceinline__ float2 mul2(float w, float2 c) { return __fmul2_rn(ma
 // slab: [j][k][CW] of this lane's position, RJ k-rows per j (4: a slab of its
 // own; more: the position's 4 x 4 corner of a window of rows); wy/wz: 12
 // weights; ax/dax/d2ax: x weights of this i.
+//
+// Separable contraction (k, then j, then i), 312 FMAs per orbital for VGH
+// (VGL 284).  The z second derivative is the one stream that reaches only
+// through (x, y) value weights, so it is not formed per row group like the
+// others (4 FMAs on every row group, then a j and an i sum): instead the
+// (ax ay)-weighted sums of the four z rows accumulate over the slabs,
+// zs[c] += sum_j (ax * ay_j) * c_jc (4 FMAs per row group), and
+// finish_z2() contracts them with d2az once per position (4 FMAs).  Every
+// product is still (weight) x (coefficient), so the error stays within a
+// few ulps of sum|w*c| (the north-star bound).
 template <int KIND, int CW, int RJ = 4>
 __device__ __forceinline__ void slab_contract(const float *__restrict__ slab, const float (&wy)[12],
                                               const float (&wz)[12], float ax, float dax, float d2ax,
-                                              float2 (&acc)[NS<KIND>::S][2]) {
-    float2 t00[2], t10[2], t01[2], t20[2], t11[2], t02[2];
+                                              float2 (&acc)[NS<KIND>::S][2], float2 (&zs)[4][2]) {
+    float2 t00[2], t10[2], t01[2], t20[2], t11[2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) t00[h] = t10[h] = t01[h] = t20[h] = t11[h] = t02[h] = make_float2(0.f, 0.f);
+    for (int h = 0; h < 2; ++h) t00[h] = t10[h] = t01[h] = t20[h] = t11[h] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         float4 c[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const float4 *>(slab + (j * RJ + k) * CW);
+        const float axy = __fmul_rn(ax, wy[j]);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const float2 c0 = h ? make_float2(c[0].z, c[0].w) : make_float2(c[0].x, c[0].y);
@@ -174,12 +185,14 @@ __device__ __forceinline__ void slab_contract(const float *__restrict__ slab, co
             t00[h] = fma2(wy[j], s0, t00[h]);
             if (KIND != SPO_KIND_V) {
                 const float2 s1 = fma2(wz[7], c3, fma2(wz[6], c2, fma2(wz[5], c1, mul2(wz[4], c0))));
-                const float2 s2 = fma2(wz[11], c3, fma2(wz[10], c2, fma2(wz[9], c1, mul2(wz[8], c0))));
                 t10[h] = fma2(wy[4 + j], s0, t10[h]);
                 t01[h] = fma2(wy[j], s1, t01[h]);
                 t20[h] = fma2(wy[8 + j], s0, t20[h]);
-                t02[h] = fma2(wy[j], s2, t02[h]);
                 if (KIND == SPO_KIND_VGH) t11[h] = fma2(wy[4 + j], s1, t11[h]);
+                zs[0][h] = fma2(axy, c0, zs[0][h]);
+                zs[1][h] = fma2(axy, c1, zs[1][h]);
+                zs[2][h] = fma2(axy, c2, zs[2][h]);
+                zs[3][h] = fma2(axy, c3, zs[3][h]);
             }
         }
     }
@@ -191,14 +204,28 @@ __device__ __forceinline__ void slab_contract(const float *__restrict__ slab, co
             acc[2][h] = fma2(ax, t10[h], acc[2][h]);
             acc[3][h] = fma2(ax, t01[h], acc[3][h]);
         }
-        if (KIND == SPO_KIND_VGL) acc[4][h] = fma2(d2ax, t00[h], fma2(ax, t20[h], fma2(ax, t02[h], acc[4][h])));
+        if (KIND == SPO_KIND_VGL) acc[4][h] = fma2(d2ax, t00[h], fma2(ax, t20[h], acc[4][h]));  // + zz: finish_z2
         if (KIND == SPO_KIND_VGH) {
             acc[4][h] = fma2(d2ax, t00[h], acc[4][h]);
             acc[5][h] = fma2(dax, t10[h], acc[5][h]);
             acc[6][h] = fma2(dax, t01[h], acc[6][h]);
             acc[7][h] = fma2(ax, t20[h], acc[7][h]);
             acc[8][h] = fma2(ax, t11[h], acc[8][h]);
-            acc[9][h] = fma2(ax, t02[h], acc[9][h]);
+        }
+    }
+}
+
+// After the four slabs: the z second derivative from the (ax ay)-weighted
+// z rows -- VGH: hzz; VGL: added to l (= hxx + hyy + hzz).
+template <int KIND>
+__device__ __forceinline__ void finish_z2(const float (&wz)[12], const float2 (&zs)[4][2],
+                                          float2 (&acc)[NS<KIND>::S][2]) {
+    if constexpr (KIND != SPO_KIND_V) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float2 zz = fma2(wz[11], zs[3][h], fma2(wz[10], zs[2][h], fma2(wz[9], zs[1][h], mul2(wz[8], zs[0][h]))));
+            if (KIND == SPO_KIND_VGH) acc[9][h] = zz;
+            if (KIND == SPO_KIND_VGL) acc[4][h] = __fadd2_rn(acc[4][h], zz);
         }
     }
 }
