@@ -442,14 +442,11 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(LW<T, KP>::CREG));
     const int g = warp - 4;
     unsigned base = 0;
-    // `issued` only grows: a value once observed (acquire) covers every plane
-    // below it, so the poll is skipped for those (saves an acquire load per plane)
-    unsigned seen = 0;
+    // (Skipping this acquire poll for planes below an `issued` value already
+    // observed is correct but measured 0.6-1.1% slower: scripts/micro/z2_ab.sh
+    // run as an A/B, profiles/r02/README.md.)
     auto await_issued = [&](unsigned x) {
-        if (x < seen) return;
-        unsigned v;
-        while ((v = ld_acquire_shared(issued)) <= x) __nanosleep(SPIN_NS);
-        seen = v;
+        while (ld_acquire_shared(issued) <= x) __nanosleep(SPIN_NS);
     };
     auto publish = [&](unsigned v) {
         __syncwarp();
