@@ -152,17 +152,18 @@ int spo_eval_lanes(int kind, int dtype, int mode, const void *table, const int32
                    int64_t lane_limit, const int64_t *out_index, int32_t *status, void *workspace,
                    int64_t workspace_bytes, void *stream);
 
-/* Workspace spo_eval wants for this request (0 = none used, -1 = bad args). */
 /*
  * Which kernel spo_eval runs for this request (no launch, no device needed):
  *   SPO_PATH_GENERIC  one-pass kernel (strict mode, no workspace, small batches)
  *   SPO_PATH_TMA      per-position TMA pipeline (spo_eval_tma.cu)
- *   SPO_PATH_LINE     line-window kernel: planes shared along grid lines, for
- *                     VGL/VGH batches of >= 1 position per grid cell, V of >= 2
+ *   SPO_PATH_LINE     line kernel: 4x4-row planes shared along grid lines
+ *                     (j0, k0), for dense batches: VGL/VGH from 4 positions
+ *                     per grid cell, V from 3 (k-power form: 1 and 2)
  *                     (spo_eval_line.cu)
- *   SPO_PATH_WINDOW   its window variant for sparse batches: (3+3) x (3+3)-row
- *                     planes shared by the positions of 3 x 3 (j0, k0) cells
- *                     (B-spline table form)
+ *   SPO_PATH_WINDOW   its window variant: (2+3) x (2+3)-row planes shared by
+ *                     the positions of 2 x 2 (j0, k0) cells, for VGL/VGH from
+ *                     0.3 positions per cell, V from 0.4 (B-spline table form)
+ *   SPO_LINE=0/1/2 in the environment forces TMA / line / window.
  * -1 on bad arguments.  All paths give bitwise identical results.
  */
 #define SPO_PATH_GENERIC 0
@@ -172,6 +173,7 @@ int spo_eval_lanes(int kind, int dtype, int mode, const void *table, const int32
 int spo_eval_path(int kind, int dtype, int mode, const int32_t *n3, int32_t nb, int32_t n_tiles, int64_t n_pos,
                   int64_t workspace_bytes);
 
+/* Workspace spo_eval wants for this request (0 = none used, -1 = bad args). */
 int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64_t n_pos);
 
 /*

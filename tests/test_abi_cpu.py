@@ -107,17 +107,24 @@ def test_eval_path_selection(lib, monkeypatch):
     monkeypatch.delenv("SPO_LINE", raising=False)
     n3 = _abi.i32x3((64, 64, 64))
     big = 1 << 40
-    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, big) == 2    # >= 1 position per cell: line
-    assert lib.spo_eval_path(1, 0, 0, n3, 128, 32, 262144, big) == 2    # VGL too
-    assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 262144, big) == 1    # V below 2 per cell: TMA
-    assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 524288, big) == 2    # V at 2 per cell: line
-    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 200000, big) == 1    # sparser: per-position TMA
+    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 1048576, big) == 2   # >= 4 positions per cell: line
+    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, big) == 3    # 0.3 .. 4 per cell: window
+    assert lib.spo_eval_path(1, 0, 0, n3, 128, 32, 262144, big) == 3    # VGL too
+    assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 786432, big) == 2    # V from 3 per cell: line
+    assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 262144, big) == 3    # V 0.4 .. 3 per cell: window
+    assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 78643, big) == 1     # V below 0.3 per cell: TMA
+    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 60000, big) == 1     # sparser: per-position TMA
     assert lib.spo_eval_path(2, 0, 1, n3, 128, 32, 262144, big) == 0    # strict: generic
     assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, 0) == 0      # no workspace: generic
-    assert lib.spo_eval_path(2, 1, 0, n3, 64, 64, 262144, big) == 2     # fp64 too
+    assert lib.spo_eval_path(2, 1, 0, n3, 64, 64, 262144, big) == 3     # fp64 too
     assert lib.spo_eval_path(2, 0, 0, n3, 96, 1, 262144, big) == 1      # rows not 512-byte multiples
     need = lib.spo_eval_workspace_bytes(2, 0, 0, 262144)
-    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, need) == 2
+    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, need) == 3
+    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, need - 1) == 1  # short workspace: TMA
+    monkeypatch.setenv("SPO_LINE", "1")
+    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, big) == 2
+    monkeypatch.setenv("SPO_LINE", "2")
+    assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 60000, big) == 3
     monkeypatch.setenv("SPO_LINE", "0")
     assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, big) == 1
     assert lib.spo_eval_path(9, 0, 0, n3, 128, 32, 262144, big) == -1
