@@ -45,20 +45,36 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every .cu to an object in parallel (one nvcc per file), then
+    link the shared library."""
+    from concurrent.futures import ThreadPoolExecutor
+
     if not force and not needs_build():
         return LIB
-    tmp = f"{LIB}.{os.getpid()}.tmp"  # concurrent builders never share a temp file
-    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-o", tmp, *SOURCES]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    tag = f"{os.getpid()}.tmp"  # concurrent builders never share a temp file
+    tmp = f"{LIB}.{tag}"
+    objs = [os.path.join(PKG, "csrc", os.path.basename(s)[:-3] + f".{tag}.o") for s in SOURCES]
+    cmds = [[nvcc(), *NVCC_FLAGS, "-c", "-o", o, s] for s, o in zip(SOURCES, objs)]
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds))
+    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
+    if all(r.returncode == 0 for r in results):
+        results.append(subprocess.run(link, capture_output=True, text=True))
+        cmds.append(link)
     log = os.path.join(PKG, "csrc", "build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stderr)
-        raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
+        for c, r in zip(cmds, results):
+            f.write(" ".join(c) + "\n" + r.stdout + r.stderr)
+    for o in objs:
+        if os.path.exists(o):
+            os.remove(o)
+    bad = [r for r in results if r.returncode != 0]
+    if bad or len(results) != len(cmds):
+        sys.stderr.write("".join(r.stderr for r in bad))
+        raise RuntimeError(f"nvcc failed; see {log}")
     os.replace(tmp, LIB)
     if verbose:
-        print(res.stderr)
+        print("".join(r.stderr for r in results))
     return LIB
 
 

@@ -64,7 +64,7 @@ constexpr unsigned SPIN_NS = 256;                // back-off of the issued / rel
 constexpr int PBATCH = 4;                        // planes issued together by the producer lanes
 constexpr int WS_HEADER = 1024;                  // ticket @0
 constexpr int NBK = 4;                           // spatial blocks per axis (as spo_eval_tma.cu)
-constexpr int MAX_AXIS = 256;                    // cell index fits 8 bits of the sort key
+constexpr int MAX_AXIS = 256;                    // cell indices fit the 10-bit fields of a plane entry
 
 template <typename T>
 struct LT;
@@ -151,8 +151,21 @@ struct LItem {
 };
 
 // ------------------------------------------------------------- prologue --
+// Sort keys, dense: lines (win == 1) order by (spatial block, j0, k0, i0) with
+// the cell coordinates taken relative to their block's first cell; windows
+// (win > 1) by (j0 / win, k0 / win, i0).  Dense keys need few bits, so the
+// radix sort runs over bits [0, key_bits) only (line_key_bits): 2-3 passes
+// instead of 4.  A non-finite position gets the all-ones key, which sorts
+// after every valid one (key_bits leaves it above the largest valid key).
+struct KeyGeom {
+    int3 nbk;   // spatial blocks per axis (lines)
+    int3 ext;   // cells per block along i, j, k (lines: ceil(n / nbk)); windows: (nx, ceil(ny / win), ceil(nz / win))
+    int win;
+};
+__device__ __forceinline__ int block_start(int b, int n, int nbk) { return (b * n + nbk - 1) / nbk; }
+
 __global__ void line_keys_kernel(GridArgs g, const double *__restrict__ pos, long long n, unsigned *__restrict__ keys,
-                                 int *__restrict__ vals, int *__restrict__ status, int3 nbk, int win) {
+                                 int *__restrict__ vals, int *__restrict__ status, KeyGeom kg) {
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
          p += (long long)gridDim.x * blockDim.x) {
         double t;
@@ -162,12 +175,15 @@ __global__ void line_keys_kernel(GridArgs g, const double *__restrict__ pos, lon
         const int k0 = map_axis(z, g.dinv[2], g.cnt[2], &t);
         unsigned key = 0xffffffffu;
         if (isfinite(x) && isfinite(y) && isfinite(z)) {
-            if (win > 1) {  // windows: all lines of a WIN x WIN window of (j0, k0) cells, in i0 order
-                key = ((unsigned)(j0 / win) << 16) | ((unsigned)(k0 / win) << 8) | (unsigned)i0;
+            if (kg.win > 1) {  // windows: all lines of a WIN x WIN window of (j0, k0) cells, in i0 order
+                key = ((unsigned)(j0 / kg.win) * kg.ext.z + (unsigned)(k0 / kg.win)) * kg.ext.x + (unsigned)i0;
             } else {
-                const unsigned b =
-                    ((i0 * nbk.x / g.n[0]) * nbk.y + j0 * nbk.y / g.n[1]) * nbk.z + k0 * nbk.z / g.n[2];
-                key = (b << 24) | ((unsigned)j0 << 16) | ((unsigned)k0 << 8) | (unsigned)i0;
+                const int bi = i0 * kg.nbk.x / g.n[0], bj = j0 * kg.nbk.y / g.n[1], bk = k0 * kg.nbk.z / g.n[2];
+                const unsigned b = (bi * kg.nbk.y + bj) * kg.nbk.z + bk;
+                const unsigned il = i0 - block_start(bi, g.n[0], kg.nbk.x);
+                const unsigned jl = j0 - block_start(bj, g.n[1], kg.nbk.y);
+                const unsigned kl = k0 - block_start(bk, g.n[2], kg.nbk.z);
+                key = ((b * kg.ext.y + jl) * kg.ext.z + kl) * kg.ext.x + il;
             }
         } else if (status) {
             atomicOr(status, 1);
@@ -219,41 +235,132 @@ __global__ void line_records_kernel(GridArgs g, const double *__restrict__ pos, 
 // every position of a win x win window of (j0, k0) cells, anchored at the
 // window's first cell (plane entry: i | J << 10 | K << 20, J = win * (j0 / win));
 // positions of one window follow each other in i0 order like a line's.
+// One warp per run, two positions per lane.  With the run sorted, a
+// position's stencil shares planes only with the position before it, and only
+// on the same line / window (`same`); the loaded range of the current line is
+// a running maximum of i0 + 3 restarted at every new line (a segmented max
+// scan), a position appends max(0, i0 + 3 - last) planes (4 on a new line),
+// and the plane numbers are the prefix sums of those counts.  That is the
+// sequential rule above, restated as two warp scans.  Non-finite positions
+// (i0 < 0, sorted last) append nothing; a run in which one precedes a finite
+// position (not produced by the sort) takes the sequential walk in lane 0.
+constexpr int RUNS_PER_BLOCK = 4;
 template <typename T>
-__global__ void line_runs_kernel(long long n, unsigned char *__restrict__ recs, int *__restrict__ plist, int win) {
+__global__ void __launch_bounds__(32 * RUNS_PER_BLOCK)
+    line_runs_kernel(long long n, unsigned char *__restrict__ recs, int *__restrict__ plist, int win) {
+    static_assert(BPL == 64, "two positions per lane");
     constexpr int RECB = LT<T>::RECB;
-    const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long b = blockIdx.x * (long long)RUNS_PER_BLOCK + w;
     if (b * BPL >= n) return;
     const int nb = (int)min((long long)BPL, n - b * BPL);
     unsigned char *rc = recs + b * BPL * RECB + 36 * sizeof(T);
-    int cj = -1, ck = -1, last = -1;
-    int next = 0;
-    for (int q = 0; q < nb; ++q) {
-        int4 *c = reinterpret_cast<int4 *>(rc + q * RECB);
-        const int4 cell = *c;
-        int s = 0;
-        if (cell.x >= 0) {
-            const int j0 = cell.y & 0xffff, k0 = cell.y >> 16, i0 = cell.x;
-            const int wj = win * (j0 / win), wk = win * (k0 / win);  // the line's / window's anchor
-            const bool same = wj == cj && wk == ck;
-            int lo;
-            if (same && i0 <= last) {
-                s = next - 1 - (last - i0);
-                lo = last + 1;
-            } else {
-                s = next;
-                lo = i0;
-            }
-            int *pl = plist + b * PL + 1;
-            for (int t = lo; t <= i0 + 3; ++t) pl[next++] = t | (wj << 10) | (wk << 20);
-            if (!same || i0 + 3 > last) last = i0 + 3;
-            cj = wj;
-            ck = wk;
-        }
-        c->z = s;
+    int *pl = plist + b * PL;
+    int i0[2], wj[2], wk[2];
+    bool ok[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int q = 2 * lane + e;
+        int4 c = make_int4(-1, 0, 0, 0);
+        if (q < nb) c = *reinterpret_cast<const int4 *>(rc + q * RECB);
+        ok[e] = c.x >= 0;
+        i0[e] = c.x;
+        const int j0 = c.y & 0xffff, k0 = c.y >> 16;
+        wj[e] = win * (j0 / win);
+        wk[e] = win * (k0 / win);
     }
-    reinterpret_cast<int4 *>(rc)->z |= next << 16;
-    plist[b * PL] = next;
+    const unsigned m0 = __ballot_sync(0xffffffffu, ok[0]), m1 = __ballot_sync(0xffffffffu, ok[1]);
+    unsigned long long valid = 0;  // bit q: position q is finite
+    for (int l = 0; l < 32; ++l)
+        valid |= (unsigned long long)((m0 >> l) & 1) << (2 * l) | (unsigned long long)((m1 >> l) & 1) << (2 * l + 1);
+    if ((valid & (valid + 1)) != 0) {  // not a prefix: the sequential walk
+        if (lane == 0) {
+            int cj = -1, ck = -1, last = -1, next = 0;
+            for (int q = 0; q < nb; ++q) {
+                int4 *c = reinterpret_cast<int4 *>(rc + q * RECB);
+                const int4 cell = *c;
+                int s = 0;
+                if (cell.x >= 0) {
+                    const int j0 = cell.y & 0xffff, k0 = cell.y >> 16, x0 = cell.x;
+                    const int aj = win * (j0 / win), ak = win * (k0 / win);
+                    const bool same = aj == cj && ak == ck;
+                    int lo;
+                    if (same && x0 <= last) {
+                        s = next - 1 - (last - x0);
+                        lo = last + 1;
+                    } else {
+                        s = next;
+                        lo = x0;
+                    }
+                    for (int t = lo; t <= x0 + 3; ++t) pl[1 + next++] = t | (aj << 10) | (ak << 20);
+                    if (!same || x0 + 3 > last) last = x0 + 3;
+                    cj = aj;
+                    ck = ak;
+                }
+                c->z = s;
+            }
+            reinterpret_cast<int4 *>(rc)->z |= next << 16;
+            pl[0] = next;
+        }
+        return;
+    }
+    // the previous position's anchor: element 0 from the lane before
+    const int pj = __shfl_up_sync(0xffffffffu, wj[1], 1), pk = __shfl_up_sync(0xffffffffu, wk[1], 1);
+    bool same[2];
+    same[0] = lane > 0 && ok[0] && wj[0] == pj && wk[0] == pk;
+    same[1] = ok[1] && wj[1] == wj[0] && wk[1] == wk[0];
+    // segmented inclusive max of i0 + 3 (a new line starts a segment)
+    const int v0 = i0[0] + 3, v1 = i0[1] + 3;
+    const bool head0 = !same[0], head1 = !same[1];
+    bool hf = head0 || head1;
+    int hv = head1 ? v1 : max(v0, v1);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int ov = __shfl_up_sync(0xffffffffu, hv, d);
+        const bool of = __shfl_up_sync(0xffffffffu, hf, d);
+        if (lane >= d) {
+            if (!hf) hv = max(hv, ov);
+            hf = hf || of;
+        }
+    }
+    const int before = __shfl_up_sync(0xffffffffu, hv, 1);  // max over the lane's predecessors' segment
+    const int run0 = head0 ? v0 : max(before, v0);
+    const int lastp[2] = {before, run0};  // `last` before each element (used only when same)
+    int cnt[2], lo[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        if (!ok[e]) {
+            cnt[e] = 0;
+            lo[e] = 0;
+        } else if (same[e] && i0[e] <= lastp[e]) {
+            lo[e] = lastp[e] + 1;
+            cnt[e] = max(0, i0[e] + 3 - lastp[e]);
+        } else {
+            lo[e] = i0[e];
+            cnt[e] = 4;
+        }
+    }
+    // exclusive prefix sum of the counts
+    int incl = cnt[0] + cnt[1];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += o;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int next = incl - cnt[0] - cnt[1];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int q = 2 * lane + e;
+        int s = 0;
+        if (ok[e]) {
+            s = (same[e] && i0[e] <= lastp[e]) ? next - 1 - (lastp[e] - i0[e]) : next;
+            for (int t = 0; t < cnt[e]; ++t) pl[1 + next + t] = (lo[e] + t) | (wj[e] << 10) | (wk[e] << 20);
+        }
+        if (q < nb) reinterpret_cast<int4 *>(rc + q * RECB)->z = s | (q == 0 ? total << 16 : 0);
+        next += cnt[e];
+    }
+    if (lane == 0) pl[0] = total;
 }
 
 // Plane slots: WIN = 1 (lines) R = LT<T>::R slots of 16 rows; windows of
@@ -701,6 +808,18 @@ static int launch_r(bool ratio, bool kp, const CUtensorMap &map, const LArgs &a,
 
 static size_t pad256(size_t b) { return (b + 255) / 256 * 256; }
 
+// Bits the radix sort must look at: the key range [0, keys) of valid
+// positions plus the all-ones key of non-finite ones, which must stay above
+// it: bit_length(keys) bits (keys itself is not a valid key).
+static int line_key_bits(const KeyGeom &kg, const TableGeom &geo) {
+    const long long blocks = kg.win > 1 ? 1 : (long long)kg.nbk.x * kg.nbk.y * kg.nbk.z;
+    const long long keys = blocks * kg.ext.x * kg.ext.y * kg.ext.z;
+    int bits = 0;
+    while (bits < 32 && (keys >> bits) != 0) ++bits;
+    (void)geo;
+    return bits < 1 ? 1 : bits;
+}
+
 }  // namespace line
 
 // Workspace of the line path: [header][keys in/out][order in/out][cub temp]
@@ -790,17 +909,25 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
         sscanf(e, "%d,%d,%d", &nbk.x, &nbk.y, &nbk.z);
         if (nbk.x * nbk.y * nbk.z > 255) nbk = make_int3(NBK, NBK, NBK);
     }
-    line_keys_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, keys_in, vals_in, status, nbk, win);
-    if (cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, vals, (int)n_pos, 0, 32, st) != cudaSuccess)
+    KeyGeom kg;
+    kg.nbk = nbk;
+    kg.win = win;
+    if (win > 1)
+        kg.ext = make_int3(geo.nx, (geo.ny + win - 1) / win, (geo.nz + win - 1) / win);
+    else
+        kg.ext = make_int3((geo.nx + nbk.x - 1) / nbk.x, (geo.ny + nbk.y - 1) / nbk.y, (geo.nz + nbk.z - 1) / nbk.z);
+    const int key_bits = line_key_bits(kg, geo);
+    line_keys_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, keys_in, vals_in, status, kg);
+    if (cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, vals, (int)n_pos, 0, key_bits, st) != cudaSuccess)
         return check_launch("spo_eval (line sort)");
     const int *order = vals.Current();  // the sorted original indices (either buffer)
-    const unsigned run_blocks = (unsigned)((n_pos + (long long)BPL * 128 - 1) / ((long long)BPL * 128));
+    const unsigned run_blocks = (unsigned)((n_pos + (long long)BPL * RUNS_PER_BLOCK - 1) / ((long long)BPL * RUNS_PER_BLOCK));
     if (dtype == SPO_F64) {
         line_records_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(g, pos, order, n_pos, recs, geo.kmul != 1);
-        line_runs_kernel<double><<<run_blocks, 128, 0, st>>>(n_pos, recs, plist, win);
+        line_runs_kernel<double><<<run_blocks, 32 * RUNS_PER_BLOCK, 0, st>>>(n_pos, recs, plist, win);
     } else {
         line_records_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(g, pos, order, n_pos, recs, geo.kmul != 1);
-        line_runs_kernel<float><<<run_blocks, 128, 0, st>>>(n_pos, recs, plist, win);
+        line_runs_kernel<float><<<run_blocks, 32 * RUNS_PER_BLOCK, 0, st>>>(n_pos, recs, plist, win);
     }
     int rc = check_launch("spo_eval (line prologue)");
     if (rc) return rc;

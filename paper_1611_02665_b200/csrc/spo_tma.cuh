@@ -28,10 +28,12 @@ inline EncodeTiledFn tensor_map_encoder() {
     return fn;
 }
 
-// box: box_lanes lanes x box_rows k-rows x box_rows j-rows of one i-plane
-// (4 x 4: one position's slab; larger: a window of several positions' slabs)
+// box: box_lanes lanes x box_rows k-rows x box_j j-rows (default box_rows) of
+// one i-plane (4 x 4: one position's slab; larger: a window of several
+// positions' slabs; 4 x 1: one row group, eval_gran_kernel)
 inline int table_tensor_map(CUtensorMap *map, const void *table, const TableGeom &geo, int dtype, int box_lanes,
-                            int box_rows = 4) {
+                            int box_rows = 4, int box_j = 0) {
+    if (box_j <= 0) box_j = box_rows;
     EncodeTiledFn encode = tensor_map_encoder();
     if (!encode) return -1;
     const cuuint64_t E = dtype == SPO_F64 ? 8 : 4;
@@ -39,7 +41,7 @@ inline int table_tensor_map(CUtensorMap *map, const void *table, const TableGeom
                           (cuuint64_t)geo.n_tiles};
     cuuint64_t strides[4] = {(cuuint64_t)geo.nb * E, (cuuint64_t)geo.nzp * geo.nb * E,
                              (cuuint64_t)geo.nyp * geo.nzp * geo.nb * E, (cuuint64_t)geo.tile_stride * E};
-    cuuint32_t box[5] = {(cuuint32_t)box_lanes, (cuuint32_t)box_rows, (cuuint32_t)box_rows, 1, 1};
+    cuuint32_t box[5] = {(cuuint32_t)box_lanes, (cuuint32_t)box_rows, (cuuint32_t)box_j, 1, 1};
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     const CUresult r =
         encode(map, dtype == SPO_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5,
@@ -162,57 +164,75 @@ __device__ __forceinline__ float2 mul2(float w, float2 c) { return __fmul2_rn(ma
 // finish_z2() contracts them with d2az once per position (4 FMAs).  Every
 // product is still (weight) x (coefficient), so the error stays within a
 // few ulps of sum|w*c| (the north-star bound).
+// The slab contraction in two steps, so that a kernel can stream a slab row
+// group by row group (eval_gran_kernel) with exactly the same arithmetic:
+// rowgroup() takes row group j (its 4 k-rows) into the j-sums t, slab_done()
+// folds the j-sums into the accumulators with the x weights of this i.
+template <int KIND, int J>
+__device__ __forceinline__ void rowgroup(const float4 (&c)[4], const float (&wy)[12], const float (&wz)[12],
+                                         float ax, float2 (&t)[5][2], float2 (&zs)[4][2]) {
+    // t[0..4] = t00, t10, t01, t20, t11
+    const float axy = __fmul_rn(ax, wy[J]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const float2 c0 = h ? make_float2(c[0].z, c[0].w) : make_float2(c[0].x, c[0].y);
+        const float2 c1 = h ? make_float2(c[1].z, c[1].w) : make_float2(c[1].x, c[1].y);
+        const float2 c2 = h ? make_float2(c[2].z, c[2].w) : make_float2(c[2].x, c[2].y);
+        const float2 c3 = h ? make_float2(c[3].z, c[3].w) : make_float2(c[3].x, c[3].y);
+        const float2 s0 = fma2(wz[3], c3, fma2(wz[2], c2, fma2(wz[1], c1, mul2(wz[0], c0))));
+        t[0][h] = fma2(wy[J], s0, t[0][h]);
+        if (KIND != SPO_KIND_V) {
+            const float2 s1 = fma2(wz[7], c3, fma2(wz[6], c2, fma2(wz[5], c1, mul2(wz[4], c0))));
+            t[1][h] = fma2(wy[4 + J], s0, t[1][h]);
+            t[2][h] = fma2(wy[J], s1, t[2][h]);
+            t[3][h] = fma2(wy[8 + J], s0, t[3][h]);
+            if (KIND == SPO_KIND_VGH) t[4][h] = fma2(wy[4 + J], s1, t[4][h]);
+            zs[0][h] = fma2(axy, c0, zs[0][h]);
+            zs[1][h] = fma2(axy, c1, zs[1][h]);
+            zs[2][h] = fma2(axy, c2, zs[2][h]);
+            zs[3][h] = fma2(axy, c3, zs[3][h]);
+        }
+    }
+}
+template <int KIND>
+__device__ __forceinline__ void slab_done(float ax, float dax, float d2ax, const float2 (&t)[5][2],
+                                          float2 (&acc)[NS<KIND>::S][2]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        acc[0][h] = fma2(ax, t[0][h], acc[0][h]);
+        if (KIND != SPO_KIND_V) {
+            acc[1][h] = fma2(dax, t[0][h], acc[1][h]);
+            acc[2][h] = fma2(ax, t[1][h], acc[2][h]);
+            acc[3][h] = fma2(ax, t[2][h], acc[3][h]);
+        }
+        if (KIND == SPO_KIND_VGL) acc[4][h] = fma2(d2ax, t[0][h], fma2(ax, t[3][h], acc[4][h]));  // + zz: finish_z2
+        if (KIND == SPO_KIND_VGH) {
+            acc[4][h] = fma2(d2ax, t[0][h], acc[4][h]);
+            acc[5][h] = fma2(dax, t[1][h], acc[5][h]);
+            acc[6][h] = fma2(dax, t[2][h], acc[6][h]);
+            acc[7][h] = fma2(ax, t[3][h], acc[7][h]);
+            acc[8][h] = fma2(ax, t[4][h], acc[8][h]);
+        }
+    }
+}
 template <int KIND, int CW, int RJ = 4>
 __device__ __forceinline__ void slab_contract(const float *__restrict__ slab, const float (&wy)[12],
                                               const float (&wz)[12], float ax, float dax, float d2ax,
                                               float2 (&acc)[NS<KIND>::S][2], float2 (&zs)[4][2]) {
-    float2 t00[2], t10[2], t01[2], t20[2], t11[2];
+    float2 t[5][2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) t00[h] = t10[h] = t01[h] = t20[h] = t11[h] = make_float2(0.f, 0.f);
+    for (int u = 0; u < 5; ++u) t[u][0] = t[u][1] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         float4 c[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const float4 *>(slab + (j * RJ + k) * CW);
-        const float axy = __fmul_rn(ax, wy[j]);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const float2 c0 = h ? make_float2(c[0].z, c[0].w) : make_float2(c[0].x, c[0].y);
-            const float2 c1 = h ? make_float2(c[1].z, c[1].w) : make_float2(c[1].x, c[1].y);
-            const float2 c2 = h ? make_float2(c[2].z, c[2].w) : make_float2(c[2].x, c[2].y);
-            const float2 c3 = h ? make_float2(c[3].z, c[3].w) : make_float2(c[3].x, c[3].y);
-            const float2 s0 = fma2(wz[3], c3, fma2(wz[2], c2, fma2(wz[1], c1, mul2(wz[0], c0))));
-            t00[h] = fma2(wy[j], s0, t00[h]);
-            if (KIND != SPO_KIND_V) {
-                const float2 s1 = fma2(wz[7], c3, fma2(wz[6], c2, fma2(wz[5], c1, mul2(wz[4], c0))));
-                t10[h] = fma2(wy[4 + j], s0, t10[h]);
-                t01[h] = fma2(wy[j], s1, t01[h]);
-                t20[h] = fma2(wy[8 + j], s0, t20[h]);
-                if (KIND == SPO_KIND_VGH) t11[h] = fma2(wy[4 + j], s1, t11[h]);
-                zs[0][h] = fma2(axy, c0, zs[0][h]);
-                zs[1][h] = fma2(axy, c1, zs[1][h]);
-                zs[2][h] = fma2(axy, c2, zs[2][h]);
-                zs[3][h] = fma2(axy, c3, zs[3][h]);
-            }
-        }
+        if (j == 0) rowgroup<KIND, 0>(c, wy, wz, ax, t, zs);
+        if (j == 1) rowgroup<KIND, 1>(c, wy, wz, ax, t, zs);
+        if (j == 2) rowgroup<KIND, 2>(c, wy, wz, ax, t, zs);
+        if (j == 3) rowgroup<KIND, 3>(c, wy, wz, ax, t, zs);
     }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        acc[0][h] = fma2(ax, t00[h], acc[0][h]);
-        if (KIND != SPO_KIND_V) {
-            acc[1][h] = fma2(dax, t00[h], acc[1][h]);
-            acc[2][h] = fma2(ax, t10[h], acc[2][h]);
-            acc[3][h] = fma2(ax, t01[h], acc[3][h]);
-        }
-        if (KIND == SPO_KIND_VGL) acc[4][h] = fma2(d2ax, t00[h], fma2(ax, t20[h], acc[4][h]));  // + zz: finish_z2
-        if (KIND == SPO_KIND_VGH) {
-            acc[4][h] = fma2(d2ax, t00[h], acc[4][h]);
-            acc[5][h] = fma2(dax, t10[h], acc[5][h]);
-            acc[6][h] = fma2(dax, t01[h], acc[6][h]);
-            acc[7][h] = fma2(ax, t20[h], acc[7][h]);
-            acc[8][h] = fma2(ax, t11[h], acc[8][h]);
-        }
-    }
+    slab_done<KIND>(ax, dax, d2ax, t, acc);
 }
 
 // After the four slabs: the z second derivative from the (ax ay)-weighted
@@ -230,51 +250,46 @@ __device__ __forceinline__ void finish_z2(const float (&wz)[12], const float2 (&
     }
 }
 
-// One i-slab for one lane: 2 fp64 orbitals, DFMA in the generic kernel's order.
-template <int KIND, int CW, int RJ = 4>
-__device__ __forceinline__ void slab_contract(const double *__restrict__ slab, const double (&wy)[12],
-                                              const double (&wz)[12], double ax, double dax, double d2ax,
-                                              double2 (&acc)[NS<KIND>::S][1]) {
-    double t00[2], t10[2], t01[2], t20[2], t11[2], t02[2];
+// One i-slab for one lane: 2 fp64 orbitals, DFMA in the generic kernel's
+// order; in the same two steps (t[0..5] = t00, t10, t01, t20, t11, t02).
+template <int KIND, int J>
+__device__ __forceinline__ void rowgroup(const double2 (&c)[4], const double (&wy)[12], const double (&wz)[12],
+                                         double (&t)[6][2]) {
 #pragma unroll
-    for (int e = 0; e < 2; ++e) t00[e] = t10[e] = t01[e] = t20[e] = t11[e] = t02[e] = 0.0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        double2 c[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const double2 *>(slab + (j * RJ + k) * CW);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const double c0 = e ? c[0].y : c[0].x, c1 = e ? c[1].y : c[1].x;
-            const double c2 = e ? c[2].y : c[2].x, c3 = e ? c[3].y : c[3].x;
-            const double s0 = __fma_rn(wz[3], c3, __fma_rn(wz[2], c2, __fma_rn(wz[1], c1, wz[0] * c0)));
-            t00[e] = __fma_rn(wy[j], s0, t00[e]);
-            if (KIND != SPO_KIND_V) {
-                const double s1 = __fma_rn(wz[7], c3, __fma_rn(wz[6], c2, __fma_rn(wz[5], c1, wz[4] * c0)));
-                const double s2 = __fma_rn(wz[11], c3, __fma_rn(wz[10], c2, __fma_rn(wz[9], c1, wz[8] * c0)));
-                t10[e] = __fma_rn(wy[4 + j], s0, t10[e]);
-                t01[e] = __fma_rn(wy[j], s1, t01[e]);
-                t20[e] = __fma_rn(wy[8 + j], s0, t20[e]);
-                t02[e] = __fma_rn(wy[j], s2, t02[e]);
-                if (KIND == SPO_KIND_VGH) t11[e] = __fma_rn(wy[4 + j], s1, t11[e]);
-            }
+    for (int e = 0; e < 2; ++e) {
+        const double c0 = e ? c[0].y : c[0].x, c1 = e ? c[1].y : c[1].x;
+        const double c2 = e ? c[2].y : c[2].x, c3 = e ? c[3].y : c[3].x;
+        const double s0 = __fma_rn(wz[3], c3, __fma_rn(wz[2], c2, __fma_rn(wz[1], c1, wz[0] * c0)));
+        t[0][e] = __fma_rn(wy[J], s0, t[0][e]);
+        if (KIND != SPO_KIND_V) {
+            const double s1 = __fma_rn(wz[7], c3, __fma_rn(wz[6], c2, __fma_rn(wz[5], c1, wz[4] * c0)));
+            const double s2 = __fma_rn(wz[11], c3, __fma_rn(wz[10], c2, __fma_rn(wz[9], c1, wz[8] * c0)));
+            t[1][e] = __fma_rn(wy[4 + J], s0, t[1][e]);
+            t[2][e] = __fma_rn(wy[J], s1, t[2][e]);
+            t[3][e] = __fma_rn(wy[8 + J], s0, t[3][e]);
+            t[5][e] = __fma_rn(wy[J], s2, t[5][e]);
+            if (KIND == SPO_KIND_VGH) t[4][e] = __fma_rn(wy[4 + J], s1, t[4][e]);
         }
     }
+}
+template <int KIND>
+__device__ __forceinline__ void slab_done(double ax, double dax, double d2ax, const double (&t)[6][2],
+                                          double2 (&acc)[NS<KIND>::S][1]) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
         double *a0 = e ? &acc[0][0].y : &acc[0][0].x;
-        *a0 = __fma_rn(ax, t00[e], *a0);
+        *a0 = __fma_rn(ax, t[0][e], *a0);
         if (KIND != SPO_KIND_V) {
             double *a1 = e ? &acc[1][0].y : &acc[1][0].x;
             double *a2 = e ? &acc[2][0].y : &acc[2][0].x;
             double *a3 = e ? &acc[3][0].y : &acc[3][0].x;
-            *a1 = __fma_rn(dax, t00[e], *a1);
-            *a2 = __fma_rn(ax, t10[e], *a2);
-            *a3 = __fma_rn(ax, t01[e], *a3);
+            *a1 = __fma_rn(dax, t[0][e], *a1);
+            *a2 = __fma_rn(ax, t[1][e], *a2);
+            *a3 = __fma_rn(ax, t[2][e], *a3);
         }
         if (KIND == SPO_KIND_VGL) {
             double *a4 = e ? &acc[4][0].y : &acc[4][0].x;
-            *a4 = __fma_rn(d2ax, t00[e], __fma_rn(ax, t20[e], __fma_rn(ax, t02[e], *a4)));
+            *a4 = __fma_rn(d2ax, t[0][e], __fma_rn(ax, t[3][e], __fma_rn(ax, t[5][e], *a4)));
         }
         if (KIND == SPO_KIND_VGH) {
             double *a4 = e ? &acc[4][0].y : &acc[4][0].x;
@@ -283,14 +298,33 @@ __device__ __forceinline__ void slab_contract(const double *__restrict__ slab, c
             double *a7 = e ? &acc[7][0].y : &acc[7][0].x;
             double *a8 = e ? &acc[8][0].y : &acc[8][0].x;
             double *a9 = e ? &acc[9][0].y : &acc[9][0].x;
-            *a4 = __fma_rn(d2ax, t00[e], *a4);
-            *a5 = __fma_rn(dax, t10[e], *a5);
-            *a6 = __fma_rn(dax, t01[e], *a6);
-            *a7 = __fma_rn(ax, t20[e], *a7);
-            *a8 = __fma_rn(ax, t11[e], *a8);
-            *a9 = __fma_rn(ax, t02[e], *a9);
+            *a4 = __fma_rn(d2ax, t[0][e], *a4);
+            *a5 = __fma_rn(dax, t[1][e], *a5);
+            *a6 = __fma_rn(dax, t[2][e], *a6);
+            *a7 = __fma_rn(ax, t[3][e], *a7);
+            *a8 = __fma_rn(ax, t[4][e], *a8);
+            *a9 = __fma_rn(ax, t[5][e], *a9);
         }
     }
+}
+template <int KIND, int CW, int RJ = 4>
+__device__ __forceinline__ void slab_contract(const double *__restrict__ slab, const double (&wy)[12],
+                                              const double (&wz)[12], double ax, double dax, double d2ax,
+                                              double2 (&acc)[NS<KIND>::S][1]) {
+    double t[6][2];
+#pragma unroll
+    for (int u = 0; u < 6; ++u) t[u][0] = t[u][1] = 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        double2 c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const double2 *>(slab + (j * RJ + k) * CW);
+        if (j == 0) rowgroup<KIND, 0>(c, wy, wz, t);
+        if (j == 1) rowgroup<KIND, 1>(c, wy, wz, t);
+        if (j == 2) rowgroup<KIND, 2>(c, wy, wz, t);
+        if (j == 3) rowgroup<KIND, 3>(c, wy, wz, t);
+    }
+    slab_done<KIND>(ax, dax, d2ax, t, acc);
 }
 
 // ---- k-power form (SPO_FORM_KPOWER tables): the 4 rows of (i, j) hold the

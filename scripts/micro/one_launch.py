@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """A few identical evaluate() launches for an ncu capture:
-    python scripts/micro/one_launch.py grid N kind density [f32|f64] [bspline|kpower] [line|tma]"""
+    python scripts/micro/one_launch.py grid N kind density [f32|f64] [bspline|kpower] [line|window|tma]"""
 import os
 import sys
 
@@ -19,7 +19,7 @@ def main():
     f64 = len(sys.argv) > 5 and sys.argv[5] == "f64"
     form = sys.argv[6] if len(sys.argv) > 6 else "bspline"
     if len(sys.argv) > 7:
-        os.environ["SPO_LINE"] = "1" if sys.argv[7] == "line" else "0"
+        os.environ["SPO_LINE"] = {"line": "1", "window": "2"}.get(sys.argv[7], "0")
     grid = unit_cell_grid(n_grid)
     dt = DeviceTable.normal_f64(grid, n, seed=1) if f64 else DeviceTable.random(grid, n, seed=1)
     if form == "kpower":
