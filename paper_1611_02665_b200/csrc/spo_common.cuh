@@ -109,6 +109,23 @@ inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 inline int dtype_size(int dtype) { return dtype == SPO_F64 ? 8 : 4; }
 
+// Launch shape of the one-thread-per-position prologue kernels (mapping,
+// weights, sort keys).  Their fp64 arithmetic is ALU-bound per SM, so a small
+// batch gets smaller blocks, enough of them to reach every SM: 256 threads
+// from 2 x 148 x 256 positions, down to 64.
+struct Grid1D {
+    unsigned blocks;
+    int threads;
+};
+inline Grid1D prologue_grid(long long n) {
+    int threads = 256;
+    while (threads > 64 && (n + threads - 1) / threads < 2 * 148) threads >>= 1;
+    long long blocks = (n + threads - 1) / threads;
+    if (blocks > 148LL * 16) blocks = 148LL * 16;
+    if (blocks < 1) blocks = 1;
+    return Grid1D{(unsigned)blocks, threads};
+}
+
 // Device table geometry shared by the eval, pack and fill kernels.
 // B-spline form: rows k' < nz + 3 per (i', j'), the stencil of cell k0 is
 // rows k0..k0+3.  k-power form (SPO_TABLE_KPOWER): rows 4*k0 + r (r < 4) hold

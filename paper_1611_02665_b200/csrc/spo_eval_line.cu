@@ -901,7 +901,7 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     if (r) return fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", r);
 
     if (cudaMemsetAsync(ws, 0, WS_HEADER, st) != cudaSuccess) return check_launch("workspace reset");
-    const long long blocks = min((n_pos + 255) / 256, 148LL * 16);
+    const Grid1D pg = prologue_grid(n_pos);
     // spatial blocks per axis: k-power rows have no halo along z, so blocks
     // flat in z cut the i/j halo re-reads (profiles/r01/nbk_sweep.txt)
     int3 nbk = geo.kmul != 1 ? make_int3(2, 2, 4) : make_int3(NBK, NBK, NBK);
@@ -917,16 +917,16 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     else
         kg.ext = make_int3((geo.nx + nbk.x - 1) / nbk.x, (geo.ny + nbk.y - 1) / nbk.y, (geo.nz + nbk.z - 1) / nbk.z);
     const int key_bits = line_key_bits(kg, geo);
-    line_keys_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, keys_in, vals_in, status, kg);
+    line_keys_kernel<<<pg.blocks, pg.threads, 0, st>>>(g, pos, n_pos, keys_in, vals_in, status, kg);
     if (cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, vals, (int)n_pos, 0, key_bits, st) != cudaSuccess)
         return check_launch("spo_eval (line sort)");
     const int *order = vals.Current();  // the sorted original indices (either buffer)
     const unsigned run_blocks = (unsigned)((n_pos + (long long)BPL * RUNS_PER_BLOCK - 1) / ((long long)BPL * RUNS_PER_BLOCK));
     if (dtype == SPO_F64) {
-        line_records_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(g, pos, order, n_pos, recs, geo.kmul != 1);
+        line_records_kernel<double><<<pg.blocks, pg.threads, 0, st>>>(g, pos, order, n_pos, recs, geo.kmul != 1);
         line_runs_kernel<double><<<run_blocks, 32 * RUNS_PER_BLOCK, 0, st>>>(n_pos, recs, plist, win);
     } else {
-        line_records_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(g, pos, order, n_pos, recs, geo.kmul != 1);
+        line_records_kernel<float><<<pg.blocks, pg.threads, 0, st>>>(g, pos, order, n_pos, recs, geo.kmul != 1);
         line_runs_kernel<float><<<run_blocks, 32 * RUNS_PER_BLOCK, 0, st>>>(n_pos, recs, plist, win);
     }
     int rc = check_launch("spo_eval (line prologue)");

@@ -27,7 +27,6 @@
 #include <cuda.h>
 
 #include <cstdlib>
-#include <type_traits>
 
 #include "spo_common.cuh"
 #include "spo_prologue.cuh"
@@ -404,215 +403,6 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
     }
 }
 
-// ------------------------------------------------- row-group streaming --
-// eval_gran_kernel: the same work items, records and contraction as
-// eval_tma_kernel for 512-byte units (one position per warp step), but each
-// warp streams its positions' table rows through a ring of NG row-group
-// granules (4 k-rows x 512 B = 2 KB, one TMA box each) instead of two 8 KB
-// slabs.  A slab stage is held from its first to its last row read, so with
-// two stages a warp has at most one slab (8 KB) in flight; a granule is
-// released as soon as its four rows are in registers, so the ring keeps
-// NG - 1 granules (14 KB at NG = 8) in flight.  That is what the sparse
-// regime needs: there every position's rows come from L2 or DRAM (no plane
-// sharing) and the warps waited on TMA latency (profiles/r02).  Bitwise the
-// same results: rowgroup() / slab_done() are slab_contract's two steps.
-constexpr int GRAN = 2048;  // bytes: 4 k-rows x 512 B
-template <typename T>
-struct GT;
-template <>
-struct GT<float> {
-    static constexpr int WARPS = 12, NG = 8;  // 12 x 16 KB of granules
-};
-template <>
-struct GT<double> {
-    static constexpr int WARPS = 8, NG = 11;  // fp64 weights need ~200 registers: 8 warps x 22 KB
-};
-
-static_assert(GT<float>::NG - 1 < 16 && GT<double>::NG - 1 < 16, "the issue cursor runs less than a position ahead");
-
-template <int KIND, typename T>
-__global__ void __launch_bounds__(GT<T>::WARPS * 32, 1)
-    eval_gran_kernel(const __grid_constant__ CUtensorMap tmap, const Args a) {
-    constexpr int WARPS = GT<T>::WARPS, NG = GT<T>::NG;
-    constexpr int BP = TT<T>::Cfg::BP;
-    constexpr int S = NS<KIND>::S;
-    constexpr int W = TT<T>::W;
-    constexpr int RECB = TT<T>::RECB;
-    constexpr int CW = 512 / (int)sizeof(T);  // lanes per unit: 32 x W
-    using AV = typename Acc<T>::V;
-    constexpr int AN = Acc<T>::N;
-    using RV = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
-
-    extern __shared__ __align__(1024) unsigned char smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned char *ring = smem + (size_t)warp * NG * GRAN;
-    unsigned long long *bars =
-        reinterpret_cast<unsigned long long *>(smem + (size_t)WARPS * NG * GRAN) + warp * (NG + 2);
-    unsigned long long *rbar = bars + NG;  // record barriers of slots 0/1
-    unsigned char *recs = smem + (size_t)WARPS * NG * GRAN + WARPS * (NG + 2) * 8 + (size_t)warp * 2 * BP * RECB;
-    ItemInfo *info = reinterpret_cast<ItemInfo *>(smem + (size_t)WARPS * NG * GRAN + WARPS * (NG + 2) * 8 +
-                                                  (size_t)WARPS * 2 * BP * RECB) + warp * 2;
-
-    if (lane == 0) {
-        for (int s = 0; s < NG + 2; ++s) mbar_init(&bars[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-
-    // Take a ticket and start the record copy of its item into `slot`.
-    auto fill = [&](int slot) {
-        if (lane == 0) {
-            const unsigned long long k = atomicAdd(a.ticket, 1u);
-            ItemInfo it;
-            it.valid = k < (unsigned long long)a.n_items;
-            if (it.valid) {
-                const long long u = (long long)k / a.nbatch;
-                const long long b = (long long)k - u * a.nbatch;
-                it.m = (int)(u / a.chunks);
-                it.c = (int)(u - (long long)it.m * a.chunks);
-                it.b0 = b * a.bp;
-                it.nb = (int)min((long long)a.bp, a.n_pos - it.b0);
-                it.G = it.nb;
-                mbar_arrive_expect_tx(&rbar[slot], (unsigned)(it.nb * RECB));
-                bulk_load(recs + slot * BP * RECB, a.recs + it.b0 * RECB, (unsigned)(it.nb * RECB), &rbar[slot]);
-            } else {
-                it.b0 = 0;
-                it.nb = it.m = it.c = it.G = 0;
-            }
-            info[slot] = it;
-        }
-        __syncwarp();
-    };
-
-    const unsigned long long policy = l2_policy(a.evict_last);
-    // Issue cursor (warp-uniform): the next granule to load is row group ig & 3
-    // of slab ig >> 2 of position ip of the item in record slot islot.  It
-    // runs NG - 1 granules ahead of the consumer, at most one position, so it
-    // moves into an item slot only after the consumer has finished (and
-    // refilled) the item that slot held before.
-    int islot = 0, ip = 0, ig = 0;
-    bool idone = false;
-    unsigned issued = 0;          // granules issued so far (granule n lives in slot n % NG)
-    unsigned rph0 = 0, rph1 = 0;  // record barrier parities (issue side waits, consumers follow)
-    auto wait_records = [&](int slot) {
-        if (slot) {
-            mbar_wait(&rbar[1], rph1);
-            rph1 ^= 1;
-        } else {
-            mbar_wait(&rbar[0], rph0);
-            rph0 ^= 1;
-        }
-    };
-    auto issue_next = [&]() {
-        if (idone) return;
-        const ItemInfo it = info[islot];
-        const int4 cell = *reinterpret_cast<const int4 *>(recs + islot * BP * RECB + ip * RECB + 36 * sizeof(T));
-        const int st = (int)(issued % NG);
-        if (lane == 0) {
-            const bool ok = cell.x >= 0;
-            mbar_arrive_expect_tx(&bars[st], ok ? (unsigned)GRAN : 0u);
-            if (ok)
-                tma_load_5d(ring + st * GRAN, &tmap, &bars[st], it.c * CW, cell.z * a.kmul, cell.y + (ig & 3),
-                            cell.x + (ig >> 2), it.m, policy);
-        }
-        ++issued;
-        if (++ig == 16) {
-            ig = 0;
-            if (++ip == it.nb) {
-                ip = 0;
-                islot ^= 1;
-                if (info[islot].valid)
-                    wait_records(islot);
-                else
-                    idone = true;
-            }
-        }
-    };
-
-    fill(0);
-    fill(1);
-    if (!info[0].valid) return;
-    wait_records(0);
-#pragma unroll 1
-    for (int q = 0; q < NG - 1; ++q) issue_next();
-
-    unsigned n = 0;  // granules consumed
-    int cslot = 0;
-    while (true) {
-        const ItemInfo it = info[cslot];
-        const unsigned char *rc = recs + cslot * BP * RECB;
-#pragma unroll 1
-        for (int p = 0; p < it.nb; ++p) {
-            T wx[12], wy[12], wz[12];
-            load_weights(rc + p * RECB, wx, wy, wz);
-            const int4 cell = *reinterpret_cast<const int4 *>(rc + p * RECB + 36 * sizeof(T));
-            AV acc[S][AN];
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-#pragma unroll
-                for (int h = 0; h < AN; ++h) zero(acc[s][h]);
-            [[maybe_unused]] AV zs[4][AN];  // fp32 z-second-derivative sums
-            if constexpr (sizeof(T) == 4) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int h = 0; h < AN; ++h) zero(zs[c][h]);
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                typename std::conditional<sizeof(T) == 4, float2[5][2], double[6][2]>::type t;
-                if constexpr (sizeof(T) == 4) {
-#pragma unroll
-                    for (int u = 0; u < 5; ++u) t[u][0] = t[u][1] = make_float2(0.f, 0.f);
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 6; ++u) t[u][0] = t[u][1] = 0.0;
-                }
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    // the granule consumed last step is out of its slot (its rows
-                    // are in registers, used by that step's FMAs): reload it
-                    __syncwarp();
-                    issue_next();
-                    const int st = (int)(n % NG);
-                    mbar_wait(&bars[st], (n / NG) & 1);
-                    const T *g = reinterpret_cast<const T *>(ring + st * GRAN) + lane * W;
-                    RV c[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const RV *>(g + k * CW);
-                    ++n;
-                    if constexpr (sizeof(T) == 4) {
-                        if (j == 0) rowgroup<KIND, 0>(c, wy, wz, wx[i], t, zs);
-                        if (j == 1) rowgroup<KIND, 1>(c, wy, wz, wx[i], t, zs);
-                        if (j == 2) rowgroup<KIND, 2>(c, wy, wz, wx[i], t, zs);
-                        if (j == 3) rowgroup<KIND, 3>(c, wy, wz, wx[i], t, zs);
-                    } else {
-                        if (j == 0) rowgroup<KIND, 0>(c, wy, wz, t);
-                        if (j == 1) rowgroup<KIND, 1>(c, wy, wz, t);
-                        if (j == 2) rowgroup<KIND, 2>(c, wy, wz, t);
-                        if (j == 3) rowgroup<KIND, 3>(c, wy, wz, t);
-                    }
-                }
-                slab_done<KIND>(wx[i], wx[4 + i], wx[8 + i], t, acc);
-            }
-            if constexpr (sizeof(T) == 4) finish_z2<KIND>(wz, zs, acc);
-            const long long gp = cell.w;  // original index
-            const long long op = a.out_index ? a.out_index[gp] : gp;
-            const long long ln = (long long)it.m * a.nb + it.c * CW + lane * W;
-            T *o = reinterpret_cast<T *>(a.out) + op * a.out_pos_stride + ln;
-            if (ln + W <= a.lane_limit)
-                store_lane<S>(o, a.out_stream_stride, acc, cell.x >= 0);
-            else if (ln < a.lane_limit)
-                store_lane_partial<S>(o, a.out_stream_stride, acc, cell.x >= 0, (int)(a.lane_limit - ln));
-        }
-        __syncwarp();
-        const bool more = info[cslot ^ 1].valid;
-        fill(cslot);  // the issue cursor has left this slot: refill it with the next ticket
-        if (!more) break;
-        cslot ^= 1;
-    }
-}
-
 // ---------------------------------------------------------------- host --
 template <typename T>
 constexpr size_t smem_bytes() {
@@ -633,24 +423,6 @@ static int launch_t(const CUtensorMap &map, const Args &a, int sms, cudaStream_t
                          (int)sm);
     eval_tma_kernel<KIND, T, CW, C, RATIO, KP><<<grid, C::WARPS * 32, sm, st>>>(map, a);
     return check_launch("spo_eval (tma) launch");
-}
-
-template <typename T>
-constexpr size_t gran_smem_bytes() {
-    return (size_t)GT<T>::WARPS * GT<T>::NG * GRAN + GT<T>::WARPS * (GT<T>::NG + 2) * 8 +
-           (size_t)GT<T>::WARPS * 2 * TT<T>::Cfg::BP * TT<T>::RECB + GT<T>::WARPS * 2 * sizeof(ItemInfo);
-}
-static_assert(gran_smem_bytes<float>() <= 232448, "shared memory budget");
-static_assert(gran_smem_bytes<double>() <= 232448, "shared memory budget");
-
-template <int KIND, typename T>
-static int launch_gran(const CUtensorMap &map, const Args &a, int sms, cudaStream_t st) {
-    constexpr size_t sm = gran_smem_bytes<T>();
-    int grid = (int)min((long long)sms, (a.n_items + GT<T>::WARPS - 1) / GT<T>::WARPS);
-    if (grid < 1) grid = 1;
-    cudaFuncSetAttribute(eval_gran_kernel<KIND, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    eval_gran_kernel<KIND, T><<<grid, GT<T>::WARPS * 32, sm, st>>>(map, a);
-    return check_launch("spo_eval (tma, row groups) launch");
 }
 
 // chunk widths in elements: 128 / 256 / 512-byte rows (the fused ratio
@@ -780,16 +552,15 @@ int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const
     unsigned char *recs = ws + WS_HEADER + ((n_pos + 15) / 16) * 16;
     if (cudaMemsetAsync(ws, 0, WS_HEADER, st) != cudaSuccess) return check_launch("workspace reset");
     {
-        long long blocks = (n_pos + 255) / 256;
-        if (blocks > 148LL * 16) blocks = 148LL * 16;
-        bucket_count_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, bucket, counts);
+        const Grid1D pg = prologue_grid(n_pos);
+        bucket_count_kernel<<<pg.blocks, pg.threads, 0, st>>>(g, pos, n_pos, bucket, counts);
         if (dtype == SPO_F64)
             prologue_records_kernel<double>
-                <<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, bucket, counts, cursors, recs, status,
+                <<<pg.blocks, pg.threads, 0, st>>>(g, pos, n_pos, bucket, counts, cursors, recs, status,
                                                    geo.kmul != 1);
         else
             prologue_records_kernel<float>
-                <<<(unsigned)blocks, 256, 0, st>>>(g, pos, n_pos, bucket, counts, cursors, recs, status,
+                <<<pg.blocks, pg.threads, 0, st>>>(g, pos, n_pos, bucket, counts, cursors, recs, status,
                                                    geo.kmul != 1);
         int rc = check_launch("spo_eval (prologue) launch");
         if (rc) return rc;
@@ -820,28 +591,8 @@ int eval_tma(int kind, int dtype, const void *table, const TableGeom &geo, const
     a.coef_stride = coef_stride;
     a.partials = ratio ? reinterpret_cast<double *>(ws + eval_tma_workspace_bytes(dtype, n_pos)) : nullptr;
 
-    // SPO_GRAN=1: 512-byte units stream row groups (eval_gran_kernel, an
-    // experiment: bitwise equal, but measured 1.5-2x slower than the slab
-    // kernel, scripts/micro/gran_ab.py, profiles/r02/gran_ab.md).
-    const char *env_gran = getenv("SPO_GRAN");  // read per call (A/B scripts flip it)
-    const bool gran = !ratio && geo.kmul == 1 && cwb == 512 && env_gran && env_gran[0] == '1';
-    int rc;
-    if (gran) {
-        map = CUtensorMap{};
-        const int rm = table_tensor_map(&map, table, geo, dtype, cw, 4, 1);
-        if (rm) return fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", rm);
-        if (dtype == SPO_F64)
-            rc = kind == SPO_KIND_V     ? launch_gran<SPO_KIND_V, double>(map, a, sms, st)
-                 : kind == SPO_KIND_VGL ? launch_gran<SPO_KIND_VGL, double>(map, a, sms, st)
-                                        : launch_gran<SPO_KIND_VGH, double>(map, a, sms, st);
-        else
-            rc = kind == SPO_KIND_V     ? launch_gran<SPO_KIND_V, float>(map, a, sms, st)
-                 : kind == SPO_KIND_VGL ? launch_gran<SPO_KIND_VGL, float>(map, a, sms, st)
-                                        : launch_gran<SPO_KIND_VGH, float>(map, a, sms, st);
-    } else {
-        rc = dtype == SPO_F64 ? launch_kind<double>(kind, cwb, ratio, map, a, sms, st)
-                              : launch_kind<float>(kind, cwb, ratio, map, a, sms, st);
-    }
+    const int rc = dtype == SPO_F64 ? launch_kind<double>(kind, cwb, ratio, map, a, sms, st)
+                                    : launch_kind<float>(kind, cwb, ratio, map, a, sms, st);
     if (rc || !ratio) return rc;
     return ratio_reduce(kind, a.partials, (long long)geo.n_tiles * a.chunks, n_pos, ratios, st);
 }

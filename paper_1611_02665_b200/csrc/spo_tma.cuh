@@ -30,7 +30,7 @@ inline EncodeTiledFn tensor_map_encoder() {
 
 // box: box_lanes lanes x box_rows k-rows x box_j j-rows (default box_rows) of
 // one i-plane (4 x 4: one position's slab; larger: a window of several
-// positions' slabs; 4 x 1: one row group, eval_gran_kernel)
+// positions' slabs)
 inline int table_tensor_map(CUtensorMap *map, const void *table, const TableGeom &geo, int dtype, int box_lanes,
                             int box_rows = 4, int box_j = 0) {
     if (box_j <= 0) box_j = box_rows;
@@ -164,8 +164,8 @@ __device__ __forceinline__ float2 mul2(float w, float2 c) { return __fmul2_rn(ma
 // finish_z2() contracts them with d2az once per position (4 FMAs).  Every
 // product is still (weight) x (coefficient), so the error stays within a
 // few ulps of sum|w*c| (the north-star bound).
-// The slab contraction in two steps, so that a kernel can stream a slab row
-// group by row group (eval_gran_kernel) with exactly the same arithmetic:
+// The slab contraction in two steps (a kernel that streams a slab row group
+// by row group keeps exactly the same arithmetic):
 // rowgroup() takes row group j (its 4 k-rows) into the j-sums t, slab_done()
 // folds the j-sums into the accumulators with the x weights of this i.
 template <int KIND, int J>
