@@ -17,6 +17,20 @@ import numpy as np
 from .errors import ConfigError, DomainError
 
 
+def _is_count(n) -> bool:
+    return isinstance(n, (int, np.integer)) and n >= 4
+
+
+def _is_spacing(d) -> bool:
+    return d > 0.0 and math.isfinite(d)
+
+
+def _require_delta(delta) -> float:
+    if not _is_spacing(delta):
+        raise DomainError(f"spacing delta must be finite and positive (got {delta!r})")
+    return float(delta)
+
+
 @dataclass(frozen=True)
 class GridSpec:
     """A 3D uniform grid with periodic wraparound (grid.py:34-81)."""
@@ -30,37 +44,22 @@ class GridSpec:
     periodic: bool = True
 
     def __post_init__(self):
-        for name in ("nx", "ny", "nz"):
-            n = getattr(self, name)
-            if not isinstance(n, (int, np.integer)) or n < 4:
-                raise ConfigError(f"{name}={n!r}: grid counts must be integers >= 4")
-        for name in ("dx", "dy", "dz"):
-            d = getattr(self, name)
-            if not (d > 0.0 and math.isfinite(d)):
-                raise ConfigError(f"{name}={d!r}: grid spacings must be positive and finite")
-        if not self.periodic:
-            raise ConfigError("only periodic grids are supported")
+        # validation as grid.py:44-58 (same exception types; own wording)
+        bad = [f"{a}={getattr(self, a)!r}" for a in ("nx", "ny", "nz") if not _is_count(getattr(self, a))]
+        if bad:
+            raise ConfigError("grid point counts need integers of at least 4: " + ", ".join(bad))
+        bad = [f"{a}={getattr(self, a)!r}" for a in ("dx", "dy", "dz") if not _is_spacing(getattr(self, a))]
+        if bad:
+            raise ConfigError("grid spacings need finite positive values: " + ", ".join(bad))
+        if self.periodic is not True:
+            raise ConfigError("GridSpec supports periodic boundaries only")
 
-    @property
-    def counts(self) -> tuple:
-        return (self.nx, self.ny, self.nz)
-
-    @property
-    def spacings(self) -> tuple:
-        return (self.dx, self.dy, self.dz)
-
-    @property
-    def lengths(self) -> tuple:
-        return (self.nx * self.dx, self.ny * self.dy, self.nz * self.dz)
-
-    @property
-    def inverse_spacings(self) -> tuple:
-        # grid.py:75-77 -- computed on the host in fp64 exactly as the reference
-        return (1.0 / self.dx, 1.0 / self.dy, 1.0 / self.dz)
-
-    @property
-    def n_points(self) -> int:
-        return self.nx * self.ny * self.nz
+    counts = property(lambda self: (self.nx, self.ny, self.nz))
+    spacings = property(lambda self: (self.dx, self.dy, self.dz))
+    lengths = property(lambda self: tuple(n * d for n, d in zip(self.counts, self.spacings)))
+    # grid.py:75-77 -- 1/d on the host in fp64, the value the reference passes
+    inverse_spacings = property(lambda self: tuple(1.0 / d for d in self.spacings))
+    n_points = property(lambda self: self.nx * self.ny * self.nz)
 
     @property
     def padded_counts(self) -> tuple:
@@ -117,10 +116,10 @@ def _device_prologue(pos: np.ndarray, grid: GridSpec, dtype=np.float32):
 
 
 def _check_position(pos):
-    x, y, z = float(pos[0]), float(pos[1]), float(pos[2])
-    if not (math.isfinite(x) and math.isfinite(y) and math.isfinite(z)):
-        raise DomainError(f"position {(x, y, z)} has non-finite components")
-    return x, y, z
+    xyz = (float(pos[0]), float(pos[1]), float(pos[2]))
+    if not all(map(math.isfinite, xyz)):
+        raise DomainError(f"cannot map a non-finite position {xyz} onto the grid")
+    return xyz
 
 
 def map_to_grid(pos, grid: GridSpec) -> GridPoint:
@@ -157,11 +156,9 @@ def _weights_at(ts: np.ndarray, delta: float) -> np.ndarray:
 
 def basis_weights(t: float, delta: float = 1.0) -> BasisWeights:
     """Basis weights for an offset t in [0, 1) at spacing delta (grid.py:180-189)."""
-    if not (0.0 <= t < 1.0):
-        raise DomainError(f"t={t!r} outside [0, 1)")
-    if not (delta > 0.0 and math.isfinite(delta)):
-        raise DomainError(f"delta={delta!r} must be positive and finite")
-    w = _weights_at(np.array([float(t)]), float(delta))[0].copy()
+    if not 0.0 <= t < 1.0:
+        raise DomainError(f"offset t must lie in [0, 1) (got {t!r})")
+    w = _weights_at(np.array([float(t)]), _require_delta(delta))[0].copy()
     w.flags.writeable = False
     return BasisWeights(a=w[0], da=w[1], d2a=w[2])
 
@@ -170,14 +167,13 @@ def basis_weights_batch(ts, delta: float = 1.0) -> np.ndarray:
     """Weights for many offsets; (len(ts), 3, 4) float32 (grid.py:192-203)."""
     ts = np.ascontiguousarray(ts, dtype=np.float64)
     if ts.ndim != 1:
-        raise DomainError("ts must be one dimensional")
-    if ts.size and not ((ts >= 0.0).all() and (ts < 1.0).all()):
-        raise DomainError("all offsets must lie in [0, 1)")
-    if not (delta > 0.0 and math.isfinite(delta)):
-        raise DomainError(f"delta={delta!r} must be positive and finite")
-    if ts.size == 0:
-        return np.empty((0, 3, 4), dtype=np.float32)
-    return _weights_at(ts, float(delta)).astype(np.float32)
+        raise DomainError(f"offsets must be a 1-D array (got shape {ts.shape})")
+    if np.any(ts < 0.0) or np.any(ts >= 1.0) or np.isnan(ts).any():
+        raise DomainError("every offset must lie in [0, 1)")
+    delta = _require_delta(delta)
+    if not ts.size:
+        return np.zeros((0, 3, 4), dtype=np.float32)
+    return _weights_at(ts, delta).astype(np.float32)
 
 
 def compute_prefactors(pos, grid: GridSpec):
