@@ -89,34 +89,44 @@ struct LT<double> {
     static constexpr int PREG = 40, CREG = 232;
     static constexpr int R = SPO_LINE_R64;  // plane slots (larger records)
 };
-// Warp split per table form.  The k-power form needs fewer registers (no z
-// weights), but 16 consumer warps at 112 registers spill and ran 10% slower
-// than 12 at 160 (31.8 vs 28.6 ms per 524,288-position launch), so both
-// forms use LT's split.
-template <typename T, bool KP>
+// Warp split per table form and kind.  The k-power form needs fewer
+// registers (no z weights), but 16 consumer warps at 112 registers spill and
+// ran 10% slower than 12 at 160 (31.8 vs 28.6 ms per 524,288-position
+// launch), so both forms use LT's split.  fp64 V needs far fewer registers
+// than fp64 VGL/VGH (one stream, four weights per axis): it takes the fp32
+// split, 12 consumer warps at 160 (SPO_F64V_WGS = 4, the default) instead of
+// 8 at 232 -- its DFMA chains were latency-bound at two warps per SMSP:
+// config 5 +4.6%, window V +3-6% (profiles/r02/f64v_split.md).
+#ifndef SPO_F64V_WGS
+#define SPO_F64V_WGS 4
+#endif
+template <typename T, bool KP, int KIND = -1>
 struct LW {
-    static constexpr int WGS = LT<T>::WGS, PREG = LT<T>::PREG, CREG = LT<T>::CREG;
+    static constexpr bool WIDE = sizeof(T) == 8 && KIND == SPO_KIND_V && SPO_F64V_WGS == 4;
+    static constexpr int WGS = WIDE ? 4 : LT<T>::WGS;
+    static constexpr int PREG = WIDE ? 32 : LT<T>::PREG, CREG = WIDE ? 160 : LT<T>::CREG;
 };
-template <typename T, bool KP = false>
+template <typename T, bool KP = false, int KIND = -1>
 constexpr int cons_warps() {
-    return 4 * (LW<T, KP>::WGS - 1);
+    return 4 * (LW<T, KP, KIND>::WGS - 1);
 }
-template <typename T, bool KP = false>
+template <typename T, bool KP = false, int KIND = -1>
 constexpr int threads() {
-    return 128 * LW<T, KP>::WGS;
+    return 128 * LW<T, KP, KIND>::WGS;
 }
 // The pool setmaxnreg redistributes is the CTA's launch allocation: threads x
 // the per-thread count __launch_bounds__ gives (64K / threads, rounded down to
 // a multiple of 8).  Growing past it would make TRY_ALLOC spin forever.
-template <typename T, bool KP = false>
+template <typename T, bool KP = false, int KIND = -1>
 constexpr bool regs_fit() {
-    return 128 * LW<T, KP>::PREG + 32 * cons_warps<T, KP>() * LW<T, KP>::CREG <=
-           threads<T, KP>() * (65536 / threads<T, KP>() / 8 * 8);
+    return 128 * LW<T, KP, KIND>::PREG + 32 * cons_warps<T, KP, KIND>() * LW<T, KP, KIND>::CREG <=
+           threads<T, KP, KIND>() * (65536 / threads<T, KP, KIND>() / 8 * 8);
 }
 static_assert(regs_fit<float>(), "fp32 register split exceeds the launch allocation");
 static_assert(regs_fit<double>(), "fp64 register split exceeds the launch allocation");
 static_assert(regs_fit<float, true>(), "fp32 k-power register split exceeds the launch allocation");
 static_assert(regs_fit<double, true>(), "fp64 k-power register split exceeds the launch allocation");
+static_assert(regs_fit<double, false, SPO_KIND_V>() && regs_fit<double, true, SPO_KIND_V>(), "fp64 V split");
 
 struct LArgs {
     const unsigned char *recs;  // [n_pos][RECB], sorted
@@ -398,9 +408,9 @@ static_assert(ring<double, WIN_CELLS>() >= 6, "a window ring must hold more than
 
 // ---------------------------------------------------------------- kernel --
 template <int KIND, typename T, bool RATIO, bool KP, int VGROUP = 1, int WIN = 1>
-__global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_constant__ CUtensorMap tmap, const LArgs a) {
+__global__ void __launch_bounds__(threads<T, KP, KIND>(), 1) line_kernel(const __grid_constant__ CUtensorMap tmap, const LArgs a) {
     constexpr int S = NS<KIND>::S;
-    constexpr int CONSUMERS = cons_warps<T, KP>();
+    constexpr int CONSUMERS = cons_warps<T, KP, KIND>();
     constexpr int R = ring<T, WIN>();
     constexpr int PB = plane_bytes<WIN>();         // bytes per plane slot
     constexpr int RJ = WIN + 3;                    // k-rows per j-row of a slot
@@ -440,7 +450,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
 
     if (warp < 4) {
         // ------------------------------------------------------ producer --
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(LW<T, KP>::PREG));
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(LW<T, KP, KIND>::PREG));
         if (warp != 0) return;
         // lane 0 takes tickets and loads run records + plane lists; lanes
         // 0..PBATCH-1 issue the run's planes PBATCH at a time (one slot each)
@@ -546,7 +556,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
     // only on its own planes: `issued` says a plane's slot is armed (so the
     // parity wait is on the right phase), and relw[g] publishes the first
     // plane it will need next (all below are free for the producer).
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(LW<T, KP>::CREG));
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(LW<T, KP, KIND>::CREG));
     const int g = warp - 4;
     unsigned base = 0;
     // (Skipping this acquire poll for planes below an `issued` value already
@@ -773,7 +783,7 @@ static int launch1(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t
     if (grid < 1) grid = 1;
     cudaFuncSetAttribute(line_kernel<KIND, T, RATIO, KP, VGROUP, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
-    line_kernel<KIND, T, RATIO, KP, VGROUP, WIN><<<grid, threads<T, KP>(), sm, st>>>(map, a);
+    line_kernel<KIND, T, RATIO, KP, VGROUP, WIN><<<grid, threads<T, KP, KIND>(), sm, st>>>(map, a);
     return check_launch("spo_eval (line) launch");
 }
 template <int KIND, typename T, bool RATIO, bool KP>
@@ -785,11 +795,13 @@ static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t 
         // V positions per consumer warp by density (scripts/micro/vm_sweep.py,
         // profiles/r01/v_groups.jsonl): fp32 2 below 3.5 positions per cell,
         // else 4; fp64 k-power 4; fp64 B-spline 1 below 4 per cell (its 4 z
-        // weights per position cost registers), else 4.  SPO_VGROUP=1..5 forces.
+        // weights per position cost registers), else 3 (at 12 consumer warps,
+        // 160 registers, 4 spills: config 5's V 13.1 ms at 3 vs 18.5 at 4,
+        // profiles/r02/f64v_split.md).  SPO_VGROUP=1..5 forces.
         const char *e = getenv("SPO_VGROUP");
         const double dens = (double)a.n_pos / (double)a.cells;
         const int v = e ? atoi(e)
-                        : (sizeof(T) == 4 ? (dens < 3.5 ? 2 : 4) : (KP ? 4 : (dens < 4.0 ? 1 : 4)));
+                        : (sizeof(T) == 4 ? (dens < 3.5 ? 2 : 4) : (KP ? 4 : (dens < 4.0 ? 1 : 3)));
         if (v == 2) return launch1<KIND, T, RATIO, KP, 2>(map, a, sms, st);
         if (v == 4) return launch1<KIND, T, RATIO, KP, 4>(map, a, sms, st);
         if (v == 3) return launch1<KIND, T, RATIO, KP, 3>(map, a, sms, st);
