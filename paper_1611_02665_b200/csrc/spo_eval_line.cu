@@ -60,7 +60,10 @@ constexpr int BOX = 16 * BOXB;                   // bytes per box (16 rows)
 constexpr int BPL = SPO_LINE_BPL;                // positions per item (run)
 constexpr int PL = 4 * BPL + 4;                  // plane-list ints per run: count, planes, pad
 constexpr int PLB = PL * 4;                      // plane-list bytes per run (16-byte multiple)
-constexpr unsigned SPIN_NS = 256;                // back-off of the issued / release polls
+#ifndef SPO_SPIN_NS
+#define SPO_SPIN_NS 256
+#endif
+constexpr unsigned SPIN_NS = SPO_SPIN_NS;        // back-off of the issued / release polls
 constexpr int PBATCH = 4;                        // planes issued together by the producer lanes
 constexpr int WS_HEADER = 1024;                  // ticket @0
 constexpr int NBK = 4;                           // spatial blocks per axis (as spo_eval_tma.cu)
