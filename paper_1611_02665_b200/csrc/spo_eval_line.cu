@@ -103,9 +103,13 @@ struct LT<double> {
 #ifndef SPO_F64V_WGS
 #define SPO_F64V_WGS 4
 #endif
+#ifndef SPO_F64VGL_WGS
+#define SPO_F64VGL_WGS 3
+#endif
 template <typename T, bool KP, int KIND = -1>
 struct LW {
-    static constexpr bool WIDE = sizeof(T) == 8 && KIND == SPO_KIND_V && SPO_F64V_WGS == 4;
+    static constexpr bool WIDE = sizeof(T) == 8 && ((KIND == SPO_KIND_V && SPO_F64V_WGS == 4) ||
+                                                     (KIND == SPO_KIND_VGL && SPO_F64VGL_WGS == 4));
     static constexpr int WGS = WIDE ? 4 : LT<T>::WGS;
     static constexpr int PREG = WIDE ? 32 : LT<T>::PREG, CREG = WIDE ? 160 : LT<T>::CREG;
 };
