@@ -88,52 +88,43 @@ struct LT<float> {
 template <>
 struct LT<double> {
     static constexpr int RECB = 36 * 8 + 16;
-    static constexpr int WGS = 3;     // 8 consumer warps: fp64 weights need ~200 registers
-    static constexpr int PREG = 40, CREG = 232;
+    // 12 consumer warps at 160 registers, as fp32.  Round 1 ran fp64 on 8 at
+    // 232 (its 36 weights are 72 registers); at two warps per SMSP the DFMA
+    // chains were latency-bound (ncu: stall `wait` 3.1 per issue, FP64 pipe
+    // 27% on config 5's V).  Measured with 12 (profiles/r02/f64v_split.md):
+    // V -21% (with groups of 3), VGL -2..5%, VGH -1%, a few spilled bytes.
+    static constexpr int WGS = 4;
+    static constexpr int PREG = 32, CREG = 160;
     static constexpr int R = SPO_LINE_R64;  // plane slots (larger records)
 };
-// Warp split per table form and kind.  The k-power form needs fewer
-// registers (no z weights), but 16 consumer warps at 112 registers spill and
-// ran 10% slower than 12 at 160 (31.8 vs 28.6 ms per 524,288-position
-// launch), so both forms use LT's split.  fp64 V needs far fewer registers
-// than fp64 VGL/VGH (one stream, four weights per axis): it takes the fp32
-// split, 12 consumer warps at 160 (SPO_F64V_WGS = 4, the default) instead of
-// 8 at 232 -- its DFMA chains were latency-bound at two warps per SMSP:
-// config 5 +4.6%, window V +3-6% (profiles/r02/f64v_split.md).
-#ifndef SPO_F64V_WGS
-#define SPO_F64V_WGS 4
-#endif
-#ifndef SPO_F64VGL_WGS
-#define SPO_F64VGL_WGS 3
-#endif
-template <typename T, bool KP, int KIND = -1>
+// Warp split per table form.  The k-power form needs fewer registers (no z
+// weights), but 16 consumer warps at 112 registers spill and ran 10% slower
+// than 12 at 160 (31.8 vs 28.6 ms per 524,288-position launch), so both
+// forms use LT's split.
+template <typename T, bool KP>
 struct LW {
-    static constexpr bool WIDE = sizeof(T) == 8 && ((KIND == SPO_KIND_V && SPO_F64V_WGS == 4) ||
-                                                     (KIND == SPO_KIND_VGL && SPO_F64VGL_WGS == 4));
-    static constexpr int WGS = WIDE ? 4 : LT<T>::WGS;
-    static constexpr int PREG = WIDE ? 32 : LT<T>::PREG, CREG = WIDE ? 160 : LT<T>::CREG;
+    static constexpr int WGS = LT<T>::WGS, PREG = LT<T>::PREG, CREG = LT<T>::CREG;
 };
-template <typename T, bool KP = false, int KIND = -1>
+template <typename T, bool KP = false>
 constexpr int cons_warps() {
-    return 4 * (LW<T, KP, KIND>::WGS - 1);
+    return 4 * (LW<T, KP>::WGS - 1);
 }
-template <typename T, bool KP = false, int KIND = -1>
+template <typename T, bool KP = false>
 constexpr int threads() {
-    return 128 * LW<T, KP, KIND>::WGS;
+    return 128 * LW<T, KP>::WGS;
 }
 // The pool setmaxnreg redistributes is the CTA's launch allocation: threads x
 // the per-thread count __launch_bounds__ gives (64K / threads, rounded down to
 // a multiple of 8).  Growing past it would make TRY_ALLOC spin forever.
-template <typename T, bool KP = false, int KIND = -1>
+template <typename T, bool KP = false>
 constexpr bool regs_fit() {
-    return 128 * LW<T, KP, KIND>::PREG + 32 * cons_warps<T, KP, KIND>() * LW<T, KP, KIND>::CREG <=
-           threads<T, KP, KIND>() * (65536 / threads<T, KP, KIND>() / 8 * 8);
+    return 128 * LW<T, KP>::PREG + 32 * cons_warps<T, KP>() * LW<T, KP>::CREG <=
+           threads<T, KP>() * (65536 / threads<T, KP>() / 8 * 8);
 }
 static_assert(regs_fit<float>(), "fp32 register split exceeds the launch allocation");
 static_assert(regs_fit<double>(), "fp64 register split exceeds the launch allocation");
 static_assert(regs_fit<float, true>(), "fp32 k-power register split exceeds the launch allocation");
 static_assert(regs_fit<double, true>(), "fp64 k-power register split exceeds the launch allocation");
-static_assert(regs_fit<double, false, SPO_KIND_V>() && regs_fit<double, true, SPO_KIND_V>(), "fp64 V split");
 
 struct LArgs {
     const unsigned char *recs;  // [n_pos][RECB], sorted
@@ -415,9 +406,9 @@ static_assert(ring<double, WIN_CELLS>() >= 6, "a window ring must hold more than
 
 // ---------------------------------------------------------------- kernel --
 template <int KIND, typename T, bool RATIO, bool KP, int VGROUP = 1, int WIN = 1>
-__global__ void __launch_bounds__(threads<T, KP, KIND>(), 1) line_kernel(const __grid_constant__ CUtensorMap tmap, const LArgs a) {
+__global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_constant__ CUtensorMap tmap, const LArgs a) {
     constexpr int S = NS<KIND>::S;
-    constexpr int CONSUMERS = cons_warps<T, KP, KIND>();
+    constexpr int CONSUMERS = cons_warps<T, KP>();
     constexpr int R = ring<T, WIN>();
     constexpr int PB = plane_bytes<WIN>();         // bytes per plane slot
     constexpr int RJ = WIN + 3;                    // k-rows per j-row of a slot
@@ -457,7 +448,7 @@ __global__ void __launch_bounds__(threads<T, KP, KIND>(), 1) line_kernel(const _
 
     if (warp < 4) {
         // ------------------------------------------------------ producer --
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(LW<T, KP, KIND>::PREG));
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(LW<T, KP>::PREG));
         if (warp != 0) return;
         // lane 0 takes tickets and loads run records + plane lists; lanes
         // 0..PBATCH-1 issue the run's planes PBATCH at a time (one slot each)
@@ -563,7 +554,7 @@ __global__ void __launch_bounds__(threads<T, KP, KIND>(), 1) line_kernel(const _
     // only on its own planes: `issued` says a plane's slot is armed (so the
     // parity wait is on the right phase), and relw[g] publishes the first
     // plane it will need next (all below are free for the producer).
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(LW<T, KP, KIND>::CREG));
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(LW<T, KP>::CREG));
     const int g = warp - 4;
     unsigned base = 0;
     // (Skipping this acquire poll for planes below an `issued` value already
@@ -790,7 +781,7 @@ static int launch1(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t
     if (grid < 1) grid = 1;
     cudaFuncSetAttribute(line_kernel<KIND, T, RATIO, KP, VGROUP, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
-    line_kernel<KIND, T, RATIO, KP, VGROUP, WIN><<<grid, threads<T, KP, KIND>(), sm, st>>>(map, a);
+    line_kernel<KIND, T, RATIO, KP, VGROUP, WIN><<<grid, threads<T, KP>(), sm, st>>>(map, a);
     return check_launch("spo_eval (line) launch");
 }
 template <int KIND, typename T, bool RATIO, bool KP>
