@@ -364,6 +364,7 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
               const void *coef = nullptr, long long coef_stride = 0, double *ratios = nullptr,
               long long ratio_bytes = 0, int win = 1);
 int line_window_cells();
+int line_v_window();
 long long eval_tma_ratio_bytes(int kind, int dtype, long long nb, long long n_tiles, long long n_pos);
 }
 
@@ -397,6 +398,13 @@ constexpr double KP_LINE_MIN_VGX = 1.0, KP_LINE_MIN_V = 2.0;
 // Which shared-plane kernel a FAST request takes: 0 = none (the per-position
 // TMA kernel), 1 = the line kernel, 3 = its window variant.  SPO_LINE=0/1/2
 // forces none / line / window (read on every call).
+// V on windows: the 2 x 1 window with V position groups (SPO_VWIN=1; read
+// per call, A/B) instead of the 2 x 2 window one position per warp.
+static bool v_window(int kind) {
+    const char *e = getenv("SPO_VWIN");
+    return kind == SPO_KIND_V && e && e[0] == '1';
+}
+
 static int line_variant(int kind, const int32_t *n3, long long n_pos, bool kpower) {
     const char *env_line = getenv("SPO_LINE");
     if (env_line) return env_line[0] == '1' ? 1 : (env_line[0] == '2' && !kpower ? 3 : 0);
@@ -475,7 +483,8 @@ static int eval_impl(int kind, int dtype, int mode, const void *table, const int
                 const int r = eval_line(kind, dtype, table, geo, g, pos, n_pos, out, out_pos_stride,
                                         out_stream_stride, reinterpret_cast<const long long *>(out_index), status,
                                         workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream), lanes,
-                                        nullptr, 0, nullptr, 0, lv == 3 ? line_window_cells() : 1);
+                                        nullptr, 0, nullptr, 0,
+                                        lv == 3 ? (v_window(kind) ? line_v_window() : line_window_cells()) : 1);
                 if (r >= 0) return r;
             }
             const int r = eval_tma(kind, dtype, table, geo, g, pos, n_pos, out, out_pos_stride, out_stream_stride,

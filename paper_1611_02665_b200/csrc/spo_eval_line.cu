@@ -165,10 +165,16 @@ struct LItem {
 // radix sort runs over bits [0, key_bits) only (line_key_bits): 2-3 passes
 // instead of 4.  A non-finite position gets the all-ones key, which sorts
 // after every valid one (key_bits leaves it above the largest valid key).
+// Window shapes: WIN = n is an n x n window of (j0, k0) cells (1: a line);
+// WIN = 10 wj + wk (wj, wk < 10, two digits) is a wj x wk one, e.g. 21 = two
+// lines along j with no halo sharing along k (planes of 5 j-rows x 4 k-rows).
+__host__ __device__ constexpr int win_j(int w) { return w > 9 ? w / 10 : w; }
+__host__ __device__ constexpr int win_k(int w) { return w > 9 ? w % 10 : w; }
+
 struct KeyGeom {
     int3 nbk;   // spatial blocks per axis (lines)
-    int3 ext;   // cells per block along i, j, k (lines: ceil(n / nbk)); windows: (nx, ceil(ny / win), ceil(nz / win))
-    int win;
+    int3 ext;   // cells per block along i, j, k (lines: ceil(n / nbk)); windows: (nx, ceil(ny / wj), ceil(nz / wk))
+    int win;    // window code (win_j / win_k)
 };
 __device__ __forceinline__ int block_start(int b, int n, int nbk) { return (b * n + nbk - 1) / nbk; }
 
@@ -183,8 +189,9 @@ __global__ void line_keys_kernel(GridArgs g, const double *__restrict__ pos, lon
         const int k0 = map_axis(z, g.dinv[2], g.cnt[2], &t);
         unsigned key = 0xffffffffu;
         if (isfinite(x) && isfinite(y) && isfinite(z)) {
-            if (kg.win > 1) {  // windows: all lines of a WIN x WIN window of (j0, k0) cells, in i0 order
-                key = ((unsigned)(j0 / kg.win) * kg.ext.z + (unsigned)(k0 / kg.win)) * kg.ext.x + (unsigned)i0;
+            if (kg.win > 1) {  // windows: all lines of a wj x wk window of (j0, k0) cells, in i0 order
+                key = ((unsigned)(j0 / win_j(kg.win)) * kg.ext.z + (unsigned)(k0 / win_k(kg.win))) * kg.ext.x +
+                      (unsigned)i0;
             } else {
                 const int bi = i0 * kg.nbk.x / g.n[0], bj = j0 * kg.nbk.y / g.n[1], bk = k0 * kg.nbk.z / g.n[2];
                 const unsigned b = (bi * kg.nbk.y + bj) * kg.nbk.z + bk;
@@ -274,8 +281,8 @@ __global__ void __launch_bounds__(32 * RUNS_PER_BLOCK)
         ok[e] = c.x >= 0;
         i0[e] = c.x;
         const int j0 = c.y & 0xffff, k0 = c.y >> 16;
-        wj[e] = win * (j0 / win);
-        wk[e] = win * (k0 / win);
+        wj[e] = win_j(win) * (j0 / win_j(win));
+        wk[e] = win_k(win) * (k0 / win_k(win));
     }
     const unsigned m0 = __ballot_sync(0xffffffffu, ok[0]), m1 = __ballot_sync(0xffffffffu, ok[1]);
     unsigned long long valid = 0;  // bit q: position q is finite
@@ -290,7 +297,7 @@ __global__ void __launch_bounds__(32 * RUNS_PER_BLOCK)
                 int s = 0;
                 if (cell.x >= 0) {
                     const int j0 = cell.y & 0xffff, k0 = cell.y >> 16, x0 = cell.x;
-                    const int aj = win * (j0 / win), ak = win * (k0 / win);
+                    const int aj = win_j(win) * (j0 / win_j(win)), ak = win_k(win) * (k0 / win_k(win));
                     const bool same = aj == cj && ak == ck;
                     int lo;
                     if (same && x0 <= last) {
@@ -376,7 +383,7 @@ __global__ void __launch_bounds__(32 * RUNS_PER_BLOCK)
 constexpr size_t SMEM_BUDGET = 232448;
 template <int WIN>
 constexpr int plane_bytes() {
-    return (WIN + 3) * (WIN + 3) * ROWB;
+    return (win_j(WIN) + 3) * (win_k(WIN) + 3) * ROWB;
 }
 template <typename T>
 constexpr size_t smem_fixed() {
@@ -398,11 +405,16 @@ constexpr size_t smem_bytes() {
 #define SPO_WIN_CELLS 2  // 2 and 3 within ~1-4% of each other, 2 ahead on most configs; 4 slower
 #endif
 constexpr int WIN_CELLS = SPO_WIN_CELLS;  // window side (cells) of the window variant
+// V on windows: two lines along j (planes of 5 j-rows x 4 k-rows), where V
+// position groups read a plane once for several positions with no k offset
+// to select (win_k = 1)
+constexpr int VWIN = 21;
 static_assert(smem_bytes<float>() <= SMEM_BUDGET, "shared memory budget");
 static_assert(smem_bytes<double>() <= SMEM_BUDGET, "shared memory budget");
 static_assert(smem_bytes<float, WIN_CELLS>() <= SMEM_BUDGET, "shared memory budget");
 static_assert(smem_bytes<double, WIN_CELLS>() <= SMEM_BUDGET, "shared memory budget");
 static_assert(ring<double, WIN_CELLS>() >= 6, "a window ring must hold more than one position's planes");
+static_assert(smem_bytes<float, VWIN>() <= SMEM_BUDGET && smem_bytes<double, VWIN>() <= SMEM_BUDGET, "budget");
 
 // ---------------------------------------------------------------- kernel --
 template <int KIND, typename T, bool RATIO, bool KP, int VGROUP = 1, int WIN = 1>
@@ -411,8 +423,9 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
     constexpr int CONSUMERS = cons_warps<T, KP>();
     constexpr int R = ring<T, WIN>();
     constexpr int PB = plane_bytes<WIN>();         // bytes per plane slot
-    constexpr int RJ = WIN + 3;                    // k-rows per j-row of a slot
-    static_assert(WIN == 1 || (!KP && VGROUP == 1), "windows: B-spline form, one position per warp");
+    constexpr int RJ = win_k(WIN) + 3;             // k-rows per j-row of a slot
+    static_assert(WIN == 1 || (!KP && (VGROUP == 1 || (KIND == SPO_KIND_V && win_k(WIN) == 1))),
+                  "windows: B-spline form; V groups only on windows without k sharing");
     constexpr int W = 16 / (int)sizeof(T);         // lanes per thread (16-byte vector)
     constexpr int RECB = LT<T>::RECB;
     constexpr int ULANES = ROWB / (int)sizeof(T);  // lanes per unit
@@ -567,7 +580,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
         __syncwarp();
         if (lane == 0) st_release_shared(&relw[g], v);
     };
-    if constexpr (KIND == SPO_KIND_V && !RATIO && VGROUP > 1 && WIN == 1) {
+    if constexpr (KIND == SPO_KIND_V && !RATIO && VGROUP > 1) {
         // V: groups of VGROUP consecutive sorted positions, group k of a run
         // to warp k mod CONSUMERS.  V has little math per plane, so a plane's
         // shared-memory read is most of its cost: the group reads each plane
@@ -603,6 +616,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
             for (int q0 = k0 * VM; q0 < it.nb; q0 += CONSUMERS * VM) {
                 T wx[VM][4], wy[VM][4], wz[VM][4];
                 unsigned s0[VM];
+                int jj[VM];  // windows along j: the position's j-row offset in the plane
                 bool live[VM];
                 long long op[VM];
                 AV acc[VM][1][AN];
@@ -620,6 +634,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                     load4(rec + 12 * sizeof(T), wy[m]);
                     load4(rec + 24 * sizeof(T), wz[m]);
                     s0[m] = base + (unsigned)(cell.z & 0xffff);
+                    jj[m] = (cell.y & 0xffff) % win_j(WIN);
                     if (live[m]) {
                         lo = min(lo, s0[m]);
                         hi = max(hi, s0[m] + 3u);
@@ -633,14 +648,23 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                     const int sl = (int)(x % R);
                     mbar_wait(&full[sl], (x / R) & 1);
                     const T *p = reinterpret_cast<const T *>(planes + (size_t)sl * PB) + lane * W;
+                    // j-row by j-row (a line: its 4; a wj x 1 window: wj + 3, each
+                    // position taking its row group j = r - jj, in increasing j
+                    // as its own slab_contract would; no k offsets to select)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
+                    for (int r = 0; r < win_j(WIN) + 3; ++r) {
                         RV c[4];
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const RV *>(p + (j * 4 + k) * BOXL);
+                        for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const RV *>(p + (r * 4 + k) * BOXL);
 #pragma unroll
-                        for (int m = 0; m < VM; ++m)
-                            if (live[m] && x - s0[m] < 4u) v_rowgroup<KP>(c, wz[m], wy[m][j], t00[m]);
+                        for (int m = 0; m < VM; ++m) {
+                            const int j = WIN == 1 ? r : r - jj[m];
+                            if (!(live[m] && x - s0[m] < 4u) || j < 0 || j > 3) continue;
+                            const T wyj = WIN == 1 ? wy[m][r]
+                                                   : (j == 0 ? wy[m][0]
+                                                             : (j == 1 ? wy[m][1] : (j == 2 ? wy[m][2] : wy[m][3])));
+                            v_rowgroup<KP>(c, wz[m], wyj, t00[m]);
+                        }
                     }
 #pragma unroll
                     for (int m = 0; m < VM; ++m)
@@ -728,7 +752,8 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
             }
             const unsigned s0 = base + (unsigned)(cell.z & 0xffff);
             // the position's 4 x 4 rows inside its slot (windows: offset by its cell in the window)
-            const int corner = WIN == 1 ? 0 : (((cell.y & 0xffff) % WIN) * RJ + (cell.y >> 16) % WIN) * BOXL;
+            const int corner =
+                WIN == 1 ? 0 : (((cell.y & 0xffff) % win_j(WIN)) * RJ + (cell.y >> 16) % win_k(WIN)) * BOXL;
             T wx[12], wy[12], wz[12];  // k-power tables: wz[0] = t_z, the rest unused
             load_weights(rec, wx, wy, wz);
 #pragma unroll
@@ -786,6 +811,19 @@ static int launch1(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t
 }
 template <int KIND, typename T, bool RATIO, bool KP>
 static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st, int win) {
+    if constexpr (!KP && KIND == SPO_KIND_V && !RATIO) {
+        if (win == VWIN) {
+            // V groups on 2 x 1 windows (SPO_VGROUP=1..5 forces)
+            const char *e = getenv("SPO_VGROUP");
+            const int v = e ? atoi(e) : (sizeof(T) == 4 ? 4 : 3);
+            if (v == 1) return launch1<KIND, T, RATIO, false, 1, VWIN>(map, a, sms, st);
+            if (v == 2) return launch1<KIND, T, RATIO, false, 2, VWIN>(map, a, sms, st);
+            if (v == 3) return launch1<KIND, T, RATIO, false, 3, VWIN>(map, a, sms, st);
+            if constexpr (4 * 5 <= ring<T, VWIN>())
+                if (v == 5) return launch1<KIND, T, RATIO, false, 5, VWIN>(map, a, sms, st);
+            return launch1<KIND, T, RATIO, false, 4, VWIN>(map, a, sms, st);
+        }
+    }
     if constexpr (!KP) {
         if (win > 1) return launch1<KIND, T, RATIO, false, 1, WIN_CELLS>(map, a, sms, st);
     }
@@ -870,6 +908,7 @@ bool eval_line_eligible(int dtype, const TableGeom &geo, long long n_pos, long l
 }
 
 int line_window_cells() { return line::WIN_CELLS; }
+int line_v_window() { return line::VWIN; }
 
 // Returns -1 when the request is not taken (the caller falls back).
 int ratio_reduce(int kind, const double *partials, long long units, long long n_pos, double *ratios,
@@ -882,7 +921,9 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     using namespace line;
     const bool ratio = ratios != nullptr;
     if (!eval_line_eligible(dtype, geo, n_pos, ws_bytes - ratio_bytes) || !aligned16(workspace)) return -1;
-    if (win != 1 && (win != WIN_CELLS || geo.kmul != 1)) return -1;  // windows: the B-spline form
+    // windows: the B-spline form; the 2 x 1 window for V only
+    if (win != 1 && ((win != WIN_CELLS && !(win == VWIN && kind == SPO_KIND_V && !ratio)) || geo.kmul != 1))
+        return -1;
     if (!tensor_map_encoder()) return -1;
     const int E = dtype == SPO_F64 ? 8 : 4;
     const int boxl = BOXB / E;
@@ -907,7 +948,7 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     int *plist = reinterpret_cast<int *>(recs + pad256((size_t)n_pos * (dtype == SPO_F64 ? LT<double>::RECB
                                                                                           : LT<float>::RECB)));
     CUtensorMap map;
-    const int r = table_tensor_map(&map, table, geo, dtype, boxl, win + 3);
+    const int r = table_tensor_map(&map, table, geo, dtype, boxl, win_k(win) + 3, win_j(win) + 3);
     if (r) return fail(SPO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", r);
 
     if (cudaMemsetAsync(ws, 0, WS_HEADER, st) != cudaSuccess) return check_launch("workspace reset");
@@ -923,7 +964,7 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     kg.nbk = nbk;
     kg.win = win;
     if (win > 1)
-        kg.ext = make_int3(geo.nx, (geo.ny + win - 1) / win, (geo.nz + win - 1) / win);
+        kg.ext = make_int3(geo.nx, (geo.ny + win_j(win) - 1) / win_j(win), (geo.nz + win_k(win) - 1) / win_k(win));
     else
         kg.ext = make_int3((geo.nx + nbk.x - 1) / nbk.x, (geo.ny + nbk.y - 1) / nbk.y, (geo.nz + nbk.z - 1) / nbk.z);
     const int key_bits = line_key_bits(kg, geo);
