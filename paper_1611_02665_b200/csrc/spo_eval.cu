@@ -389,30 +389,32 @@ extern "C" int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64
 // (j0, k0) cells: +4% at 0.3/cell, +15-20% at 0.5-1/cell over the
 // per-position kernel, +1-5% over the line kernel up to 2.4/cell); the line
 // kernel from LINE_MIN_* (many positions per line: its V position groups
-// and fewer plane loads per slot pay).  k-power tables: no window variant
-// (rows have no z halo), the line kernel from 1 (VGL/VGH) / 2 (V) per cell.
-constexpr double WINDOW_MIN_VGX = 0.3, WINDOW_MIN_V = 0.4;
-constexpr double LINE_MIN_VGX = 4.0, LINE_MIN_V = 3.0;
+// and fewer plane loads per slot pay).  V from VWIN_MIN_V per cell to the
+// line kernel: the 2 x 1 window (planes of two lines along j) with V
+// position groups, 7-16% ahead of both the 2 x 2 window and the line kernel
+// there (profiles/r02/v_window.md).  k-power tables: no window variant (rows
+// have no z halo), the line kernel from 1 (VGL/VGH) / 2 (V) per cell.
+constexpr double WINDOW_MIN_VGX = 0.3, WINDOW_MIN_V = 0.4, VWIN_MIN_V = 1.5;
+constexpr double LINE_MIN_VGX = 4.0, LINE_MIN_V32 = 3.5, LINE_MIN_V64 = 4.0;
 constexpr double KP_LINE_MIN_VGX = 1.0, KP_LINE_MIN_V = 2.0;
 
 // Which shared-plane kernel a FAST request takes: 0 = none (the per-position
-// TMA kernel), 1 = the line kernel, 3 = its window variant.  SPO_LINE=0/1/2
-// forces none / line / window (read on every call).
-// V on windows: the 2 x 1 window with V position groups (SPO_VWIN=1; read
-// per call, A/B) instead of the 2 x 2 window one position per warp.
-static bool v_window(int kind) {
-    const char *e = getenv("SPO_VWIN");
-    return kind == SPO_KIND_V && e && e[0] == '1';
-}
-
-static int line_variant(int kind, const int32_t *n3, long long n_pos, bool kpower) {
-    const char *env_line = getenv("SPO_LINE");
-    if (env_line) return env_line[0] == '1' ? 1 : (env_line[0] == '2' && !kpower ? 3 : 0);
+// TMA kernel), 1 = the line kernel, 3 = its 2 x 2 window variant, 4 = the
+// 2 x 1 window with V position groups (V only).  SPO_LINE=0/1/2 forces none
+// / line / a window (read on every call; SPO_VWIN=0/1 then picks which for V).
+static int line_variant(int kind, int dtype, const int32_t *n3, long long n_pos, bool kpower) {
     const double dens = (double)n_pos / ((double)n3[0] * n3[1] * n3[2]);
     const bool v = kind == SPO_KIND_V;
+    auto window = [&]() {
+        const char *e = getenv("SPO_VWIN");
+        const bool vw = v && (e ? e[0] == '1' : dens >= VWIN_MIN_V);
+        return vw ? 4 : 3;
+    };
+    const char *env_line = getenv("SPO_LINE");
+    if (env_line) return env_line[0] == '1' ? 1 : (env_line[0] == '2' && !kpower ? window() : 0);
     if (kpower) return dens >= (v ? KP_LINE_MIN_V : KP_LINE_MIN_VGX) ? 1 : 0;
-    if (dens >= (v ? LINE_MIN_V : LINE_MIN_VGX)) return 1;
-    return dens >= (v ? WINDOW_MIN_V : WINDOW_MIN_VGX) ? 3 : 0;
+    if (dens >= (v ? (dtype == SPO_F64 ? LINE_MIN_V64 : LINE_MIN_V32) : LINE_MIN_VGX)) return 1;
+    return dens >= (v ? WINDOW_MIN_V : WINDOW_MIN_VGX) ? window() : 0;
 }
 
 // lane_limit < 0: every table lane is stored and `out` must be memory of the
@@ -478,13 +480,13 @@ static int eval_impl(int kind, int dtype, int mode, const void *table, const int
                 g.delta[ax] = delta3[ax];
                 g.n[ax] = n3[ax];
             }
-            const int lv = line_variant(kind, n3, n_pos, kpower);
+            const int lv = line_variant(kind, dtype, n3, n_pos, kpower);
             if (lv) {
                 const int r = eval_line(kind, dtype, table, geo, g, pos, n_pos, out, out_pos_stride,
                                         out_stream_stride, reinterpret_cast<const long long *>(out_index), status,
                                         workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream), lanes,
                                         nullptr, 0, nullptr, 0,
-                                        lv == 3 ? (v_window(kind) ? line_v_window() : line_window_cells()) : 1);
+                                        lv == 4 ? line_v_window() : (lv == 3 ? line_window_cells() : 1));
                 if (r >= 0) return r;
             }
             const int r = eval_tma(kind, dtype, table, geo, g, pos, n_pos, out, out_pos_stride, out_stream_stride,
@@ -589,8 +591,8 @@ extern "C" int spo_eval_path(int kind, int dtype, int mode, const int32_t *n3, i
     if (mode != SPO_MODE_FAST || workspace_bytes <= 0) return SPO_PATH_GENERIC;
     const char *env_tma = getenv("SPO_TMA");
     if (env_tma && env_tma[0] == '0') return SPO_PATH_GENERIC;
-    const int lv = line_variant(kind, n3, n_pos, kpower);
-    if (lv && eval_line_eligible(dtype, geo, n_pos, workspace_bytes)) return lv == 3 ? SPO_PATH_WINDOW : SPO_PATH_LINE;
+    const int lv = line_variant(kind, dtype, n3, n_pos, kpower);
+    if (lv && eval_line_eligible(dtype, geo, n_pos, workspace_bytes)) return lv >= 3 ? SPO_PATH_WINDOW : SPO_PATH_LINE;
     if (workspace_bytes >= eval_tma_workspace_bytes(dtype, n_pos) && n_pos < (1LL << 31)) return SPO_PATH_TMA;
     return SPO_PATH_GENERIC;
 }

@@ -813,9 +813,12 @@ template <int KIND, typename T, bool RATIO, bool KP>
 static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st, int win) {
     if constexpr (!KP && KIND == SPO_KIND_V && !RATIO) {
         if (win == VWIN) {
-            // V groups on 2 x 1 windows (SPO_VGROUP=1..5 forces)
+            // V groups on 2 x 1 windows (profiles/r02/v_window.md): fp32 2
+            // positions per warp below 1.75 per cell, else 4; fp64 3.
+            // SPO_VGROUP=1..5 forces.
             const char *e = getenv("SPO_VGROUP");
-            const int v = e ? atoi(e) : (sizeof(T) == 4 ? 4 : 3);
+            const double dens = (double)a.n_pos / (double)a.cells;
+            const int v = e ? atoi(e) : (sizeof(T) == 4 ? (dens < 1.75 ? 2 : 4) : 3);
             if (v == 1) return launch1<KIND, T, RATIO, false, 1, VWIN>(map, a, sms, st);
             if (v == 2) return launch1<KIND, T, RATIO, false, 2, VWIN>(map, a, sms, st);
             if (v == 3) return launch1<KIND, T, RATIO, false, 3, VWIN>(map, a, sms, st);
