@@ -718,9 +718,29 @@ def run_config5(args, d):
     allpos = device_walker_positions(1, 0, walkers, 0, "v", cfg.moves, cfg.grid, device=d.dev)
     P_all = allpos.shape[0]
     # launch chunks of the global position sequence; kind by index mod 14
-    chunk = args.chunk or 262144
     kinds = ("v", "vgl", "vgh")
     S = {"v": 1, "vgl": 5, "vgh": 10}
+    n_local = hi - lo
+    npad = -(-N // 2) * 2  # PeerGather's row length (fp64 lane quantum 2)
+
+    def buffer_bytes(c):
+        """Largest buffer set alive at once for chunks of c positions: the
+        eval leg's local outputs or (root) the gather buffers [cap][S][N]."""
+        cap = {"v": -(-c * 12 // 14) + 1, "vgl": c // 14 + 1, "vgh": c // 14 + 1}
+        return max(sum(cap[k] * S[k] * lanes * 8 for k in kinds) for lanes in (table.lanes, npad))
+
+    chunk = args.chunk
+    if chunk <= 0:
+        # auto: the largest launch whose buffers leave 24 GB of HBM free.  V is
+        # 12 of every 14 positions and runs faster the denser its launch (the
+        # line kernel shares stencil planes between positions: 16 V positions
+        # per cell in one launch of the whole step against 2 in 262,144-position
+        # chunks), so the whole step goes in one launch per kind when the full-N
+        # outputs of all its positions fit (132 GB of the root's 180).
+        free, _ = torch.cuda.mem_get_info(d.dev)
+        chunk = next((c for c in (P_all, 1 << 20, 1 << 19) if c <= P_all and buffer_bytes(c) + (24 << 30) <= free),
+                     min(P_all, 1 << 18))
+        chunk = -int(d.max(float(-chunk)))  # every rank launches the same chunks: the smallest choice
     idx = torch.arange(P_all, device=d.dev) % 14
     sel = {"v": idx < 12, "vgl": idx == 12, "vgh": idx == 13}
     plan = []  # [(kind, positions tensor)] per chunk
@@ -731,9 +751,8 @@ def run_config5(args, d):
     del allpos, idx, sel
     cap = {k: max(p.shape[0] for kk, p in plan if kk == k) for k in kinds}
     counts = {k: sum(p.shape[0] for kk, p in plan if kk == k) for k in kinds}
-    n_local = hi - lo
     local_out = {k: torch.empty((cap[k], S[k], table.lanes), dtype=torch.float64, device=d.dev) for k in kinds}
-    gathers = {k: PeerGather(part, k, cap[k], np.float64, root=0, device=d.dev) for k in kinds}
+    gathers = {}
     stream = torch.cuda.current_stream(d.dev)
     v_ev = []
 
@@ -765,7 +784,6 @@ def run_config5(args, d):
                     gather_ev.append(e)
 
     eval_ms, clocks = timed_steps(d, eval_step, args.steps, args.warmup, d.local)
-    peer_ms, peer_clocks = timed_steps(d, peer_step, args.steps, args.warmup, d.local)
     res_nccl = None
     if not args.no_extra and not d.shared:  # ranks sharing a GPU run gloo: no NCCL baseline
         nsteps = max(2, min(args.steps, 5))
@@ -775,6 +793,13 @@ def run_config5(args, d):
         res_nccl = {"ms_per_step": nccl_ms / nsteps, "gather_ms_per_step": g_ms,
                     "value": P_all * N * nsteps / (nccl_ms / 1e3),
                     "what": "evaluate into local buffers + NCCL all-gather of padded blocks + permute on rank 0"}
+    # the eval and NCCL legs' local outputs go before the gather buffers come
+    # (at one rank both are the full [cap][S][N] set)
+    torch.cuda.synchronize(d.dev)
+    local_out.clear()
+    torch.cuda.empty_cache()
+    gathers.update({k: PeerGather(part, k, cap[k], np.float64, root=0, device=d.dev) for k in kinds})
+    peer_ms, peer_clocks = timed_steps(d, peer_step, args.steps, args.warmup, d.local)
     units = P_all * N * args.steps
     avg_v = sum(s.elapsed_time(e) for s, e in v_ev) / max(1, len(v_ev))
     v_launch = cap["v"]

@@ -63,7 +63,7 @@ def parse_raw(rep):
     return rec
 
 
-def capture(tag, extra):
+def capture(tag, extra, replay="kernel"):
     os.makedirs(OUT, exist_ok=True)
     base = [sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1", "--warmup", "3", "--no-cpu",
             "--no-e2e", "--no-extra", *extra]
@@ -77,7 +77,8 @@ def capture(tag, extra):
     path = line["config"].get("path") or line["config"].get("path_v")
     rep = os.path.join(OUT, f"prof_{tag}")
     cmd = ["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on", "-k",
-           f"regex:{KERNEL_RE[path]}", "-c", "1", "-o", rep, "-f", *base]
+           f"regex:{KERNEL_RE[path]}", "-c", "1", "-o", rep, "-f",
+           *(["--replay-mode", "application"] if replay == "application" else []), *base]
     r = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
     with open(os.path.join(OUT, f"ncu_{tag}.log"), "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout[-20000:] + r.stderr[-20000:])
@@ -117,12 +118,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tag")
     ap.add_argument("--merge", nargs="*")
+    ap.add_argument("--replay", default="kernel", choices=("kernel", "application"),
+                    help="application: launches whose buffers ncu's kernel replay cannot save (config 5)")
     ap.add_argument("extra", nargs=argparse.REMAINDER)
     a = ap.parse_args()
     if a.merge:
         return merge(a.merge)
     extra = a.extra[1:] if a.extra[:1] == ["--"] else a.extra
-    capture(a.tag or "capture", extra)
+    capture(a.tag or "capture", extra, a.replay)
 
 
 if __name__ == "__main__":
