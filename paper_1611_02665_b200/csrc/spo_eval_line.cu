@@ -150,6 +150,7 @@ struct LArgs {
     double dz, dz2;
     int rotate;                 // rotate the run's positions over the consumer warps
     int dynamic;                // consumers take positions from a shared per-run counter
+    int vuni;                   // V groups: the unrolled same-cell path (SPO_VUNI=0 disables, for A/B)
     long long cells;            // grid cells (positions per cell pick the V group size)
 };
 
@@ -643,6 +644,37 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                     for (int h = 0; h < AN; ++h) zero(acc[m][0][h]);
                     t00[m][0] = t00[m][1] = TV{};
                 }
+                // Dense batches: the group's positions mostly sit in one cell (same
+                // first plane, same row offset), so all of them take the same four
+                // planes row group by row group -- unrolled with no per-position
+                // tests (the general loop below spends ~60% of its instructions on
+                // them: ncu on config 5's V, profiles/r02/f64v_uniform.md).  Each
+                // position sees exactly the general loop's sequence (bitwise).
+                bool uni = a.vuni && live[0];
+#pragma unroll
+                for (int m = 1; m < VM; ++m) uni = uni && live[m] && s0[m] == s0[0] && (WIN == 1 || jj[m] == jj[0]);
+                if (uni) {
+                    await_issued(hi);  // planes are armed in order: lo .. hi are all issued
+                    const int roff = WIN == 1 ? 0 : jj[0] * 4 * BOXL;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const unsigned x = lo + (unsigned)i;
+                        const int sl = (int)(x % R);
+                        mbar_wait(&full[sl], (x / R) & 1);
+                        const T *p = reinterpret_cast<const T *>(planes + (size_t)sl * PB) + roff + lane * W;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            RV c[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const RV *>(p + (j * 4 + k) * BOXL);
+#pragma unroll
+                            for (int m = 0; m < VM; ++m) v_rowgroup<KP>(c, wz[m], wy[m][j], t00[m]);
+                        }
+#pragma unroll
+                        for (int m = 0; m < VM; ++m) v_plane_done(wx[m][i], t00[m], acc[m]);
+                    }
+                    lo = 0xffffffffu;  // done: skip the general loop
+                }
                 for (unsigned x = lo; lo != 0xffffffffu && x <= hi; ++x) {
                     await_issued(x);
                     const int sl = (int)(x % R);
@@ -1015,6 +1047,8 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     // rotated static assignment).  +0.3-1% (scripts/micro/dynamic_ab.sh)
     const char *env_dyn = getenv("SPO_DYNAMIC");
     a.dynamic = !(env_dyn && env_dyn[0] == '0');
+    const char *env_uni = getenv("SPO_VUNI");
+    a.vuni = !(env_uni && env_uni[0] == '0');
     a.dz = g.dinv[2];
     a.dz2 = 2.0 * g.dinv[2] * g.dinv[2];
 
