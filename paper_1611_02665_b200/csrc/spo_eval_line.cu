@@ -151,6 +151,8 @@ struct LArgs {
     int rotate;                 // rotate the run's positions over the consumer warps
     int dynamic;                // consumers take positions from a shared per-run counter
     int vuni;                   // V groups: the unrolled same-cell path (SPO_VUNI=0 disables, for A/B)
+    int pspin;                  // producer mbarrier waits: 1 = tight try_wait spin, 0 = test + nanosleep back-off
+    int vdyn;                   // V groups taken from a shared per-run counter (SPO_VDYN=0: rotated static)
     long long cells;            // grid cells (positions per cell pick the V group size)
 };
 
@@ -386,21 +388,46 @@ template <int WIN>
 constexpr int plane_bytes() {
     return (win_j(WIN) + 3) * (win_k(WIN) + 3) * ROWB;
 }
-template <typename T>
+// Run slots (NRS): how many runs' records + plane lists a CTA holds.  Two let
+// the producer fetch run r+1 while the consumers evaluate run r.  The V group
+// kernels on lines take three (SPO_LINE_NRS_V; a V run is short, ~1.8 groups
+// per warp, and with the groups handed out dynamically a third slot is worth
+// 2.5% on config 5's V; four measured the same as three; the window rings
+// have no room: scripts/micro/vdyn_ab.sh, profiles/r02/v_dynamic.md).
+#ifndef SPO_LINE_NRS_V
+#define SPO_LINE_NRS_V 3
+#endif
+template <typename T, int NRS = 2>
 constexpr size_t smem_fixed() {
-    return 2 * (size_t)BPL * LT<T>::RECB + 2 * (size_t)PLB + 2 * sizeof(LItem) + 4 * 8;
+    return NRS * ((size_t)BPL * LT<T>::RECB + (size_t)PLB + sizeof(LItem) + 2 * 8);
 }
-template <typename T, int WIN>
+template <typename T, int WIN, int NRS = 2>
 constexpr int ring() {
-    return WIN == 1 ? LT<T>::R : (int)((SMEM_BUDGET - smem_fixed<T>()) / (plane_bytes<WIN>() + 16));
+    constexpr int fit = (int)((SMEM_BUDGET - smem_fixed<T, NRS>()) / (plane_bytes<WIN>() + 16));
+    return WIN == 1 ? (LT<T>::R < fit ? LT<T>::R : fit) : fit;
 }
-template <typename T, int WIN = 1>
+// as many run slots (<= SPO_LINE_NRS_V) as leave the V group its ring: the 4 x
+// VGROUP planes a group may span, the rest of the producer's last batch
+// (ring_min below) and a few to load ahead
+template <int KIND, typename T, int VGROUP, int WIN>
+constexpr int rec_slots() {
+    if (!(KIND == SPO_KIND_V && VGROUP > 1)) return 2;
+    if (SPO_LINE_NRS_V >= 4 && ring<T, WIN, 4>() >= 4 * VGROUP + PBATCH + 3) return 4;
+    if (SPO_LINE_NRS_V >= 3 && ring<T, WIN, 3>() >= 4 * VGROUP + PBATCH + 3) return 3;
+    return 2;
+}
+// The smallest deadlock-free ring: the warp furthest behind holds planes from
+// lo on and may wait for plane lo + 4 VGROUP - 1; the producer arms planes in
+// batches of PBATCH and waits for ring space for a whole batch, so the batch
+// that holds that plane can reach PBATCH - 1 planes past it.
+constexpr int ring_min(int vgroup) { return 4 * vgroup + PBATCH - 1; }
+template <typename T, int WIN = 1, int NRS = 2>
 constexpr size_t smem_planes() {
-    return (size_t)ring<T, WIN>() * plane_bytes<WIN>();
+    return (size_t)ring<T, WIN, NRS>() * plane_bytes<WIN>();
 }
-template <typename T, int WIN = 1>
+template <typename T, int WIN = 1, int NRS = 2>
 constexpr size_t smem_bytes() {
-    return smem_planes<T, WIN>() + smem_fixed<T>() + 2 * (size_t)ring<T, WIN>() * 8;
+    return smem_planes<T, WIN, NRS>() + smem_fixed<T, NRS>() + 2 * (size_t)ring<T, WIN, NRS>() * 8;
 }
 #ifndef SPO_WIN_CELLS
 #define SPO_WIN_CELLS 2  // 2 and 3 within ~1-4% of each other, 2 ahead on most configs; 4 slower
@@ -422,7 +449,8 @@ template <int KIND, typename T, bool RATIO, bool KP, int VGROUP = 1, int WIN = 1
 __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_constant__ CUtensorMap tmap, const LArgs a) {
     constexpr int S = NS<KIND>::S;
     constexpr int CONSUMERS = cons_warps<T, KP>();
-    constexpr int R = ring<T, WIN>();
+    constexpr int NRS = rec_slots<KIND, T, VGROUP, WIN>();  // run slots (records + plane list)
+    constexpr int R = ring<T, WIN, NRS>();
     constexpr int PB = plane_bytes<WIN>();         // bytes per plane slot
     constexpr int RJ = win_k(WIN) + 3;             // k-rows per j-row of a slot
     static_assert(WIN == 1 || (!KP && (VGROUP == 1 || (KIND == SPO_KIND_V && win_k(WIN) == 1))),
@@ -437,22 +465,23 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
 
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char *planes = smem;
-    unsigned char *recs = smem + smem_planes<T, WIN>();
-    int *plists = reinterpret_cast<int *>(recs + 2 * BPL * RECB);
-    LItem *info = reinterpret_cast<LItem *>(plists + 2 * PL);
-    unsigned long long *full = reinterpret_cast<unsigned long long *>(info + 2);
+    unsigned char *recs = smem + smem_planes<T, WIN, NRS>();
+    int *plists = reinterpret_cast<int *>(recs + NRS * BPL * RECB);
+    LItem *info = reinterpret_cast<LItem *>(plists + NRS * PL);
+    unsigned long long *full = reinterpret_cast<unsigned long long *>(info + NRS);
     unsigned *relw = reinterpret_cast<unsigned *>(full + R);  // [CONSUMERS]: first plane each warp still needs
     unsigned *issued = relw + CONSUMERS;                      // planes armed so far
     unsigned long long *rfull = full + 2 * R;
-    unsigned long long *rempty = rfull + 2;
-    unsigned *qnext = issued + 1;                             // [2]: next position of each record slot's run
-    static_assert((CONSUMERS + 3) * 4 <= R * 8, "release words fit");
+    unsigned long long *rempty = rfull + NRS;
+    unsigned *qnext = issued + 1;                             // [NRS]: next position of each run slot's run
+    static_assert((CONSUMERS + 1 + NRS) * 4 <= R * 8, "release words fit");
+    static_assert(ring_min(1) <= R, "a position's planes and the producer's batch must fit the ring");
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x < CONSUMERS + 3) relw[threadIdx.x] = 0;  // and issued, qnext
+    if (threadIdx.x < CONSUMERS + 1 + NRS) relw[threadIdx.x] = 0;  // and issued, qnext
     if (threadIdx.x == 0) {
         for (int s = 0; s < R; ++s) mbar_init(&full[s], 1);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < NRS; ++s) {
             mbar_init(&rfull[s], 1);
             mbar_init(&rempty[s], CONSUMERS);
         }
@@ -467,6 +496,19 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
         // lane 0 takes tickets and loads run records + plane lists; lanes
         // 0..PBATCH-1 issue the run's planes PBATCH at a time (one slot each)
         const unsigned long long policy = l2_policy(a.evict_last);
+        // The producer's mbarrier waits: a try_wait spin (default).  It takes
+        // issue slots from the three consumer warps on its scheduler (ncu on
+        // config 5's V: 2.7e8 spin iterations per launch, 14% of all
+        // instructions executed), but a nanosleep back-off (SPO_PSPIN=0)
+        // reacts later and measured slower; the consumers' dynamic position /
+        // group counters absorb the imbalance instead.
+        auto pwait = [&](unsigned long long *bar, unsigned par) {
+            if (a.pspin) {
+                mbar_wait(bar, par);
+                return;
+            }
+            while (!mbar_test(bar, par)) __nanosleep(SPIN_NS);
+        };
         auto fill = [&](int slot) {  // lane 0
             const unsigned long long k = atomicAdd(a.ticket, 1u);
             LItem it;
@@ -497,26 +539,25 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
         auto poll = [&](bool block) {  // lane 0
             if (pend < 0) return;
             if (block)
-                mbar_wait(&rempty[pend], pend_par);
+                pwait(&rempty[pend], pend_par);
             else if (!mbar_test(&rempty[pend], pend_par))
                 return;
             fill(pend);
             pend = -1;
         };
         if (lane == 0) {
-            fill(0);
-            fill(1);
+            for (int s = 0; s < NRS; ++s) fill(s);
         }
         __syncwarp();
         unsigned base = 0;  // plane number of the current run's first plane
         for (int r = 0;; ++r) {
-            const int slot = r & 1;
-            mbar_wait(&rfull[slot], (r >> 1) & 1);
+            const int slot = r % NRS;
+            pwait(&rfull[slot], (r / NRS) & 1);
             const LItem it = info[slot];
             if (!it.valid) break;
             if (r >= 1) {
-                pend = slot ^ 1;  // item r-1's slot, for item r+1
-                pend_par = ((r - 1) >> 1) & 1;
+                pend = (r - 1) % NRS;  // item r-1's slot, for item r-1+NRS
+                pend_par = ((r - 1) / NRS) & 1;
             }
             const int *pl = plists + slot * PL;
             const int count = pl[0];
@@ -542,7 +583,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                     const unsigned n = s / R;
                     // the slot's previous plane has landed (the producer observes
                     // every plane in order, so the parity cannot alias)
-                    if (n > 0) mbar_wait(&full[sl], (n - 1) & 1);
+                    if (n > 0) pwait(&full[sl], (n - 1) & 1);
                     const int c = pl[1 + t];
                     mbar_arrive_expect_tx(&full[sl], PB);
                     tma_load_5d(planes + (size_t)sl * PB, &tmap, &full[sl], lt, a.kmul * ((c >> 20) & 0x3ff),
@@ -590,12 +631,12 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
         // (v_rowgroup, bitwise the one-position sequence).  Ring safety as
         // below: the warp publishes lo, and hi <= lo + 4 VGROUP - 1 < lo + R.
         constexpr int VM = VGROUP;
-        static_assert(4 * VM <= R, "a group's planes must fit the ring");
+        static_assert(ring_min(VM) <= R, "a group's planes and the producer's batch must fit the ring");
         using RV = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
         using TV = typename std::conditional<sizeof(T) == 4, float2, double>::type;
         for (int r = 0;; ++r) {
-            const int slot = r & 1;
-            mbar_wait(&rfull[slot], (r >> 1) & 1);
+            const int slot = r % NRS;
+            mbar_wait(&rfull[slot], (r / NRS) & 1);
             const LItem it = info[slot];
             if (!it.valid) break;
             const unsigned char *rc = recs + slot * BPL * RECB;
@@ -610,11 +651,20 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
             // the same share of groups over consecutive runs (64 / VM groups do
             // not divide evenly among the warps)
             const int rot = a.rotate ? (int)((long long)r * (BPL / VM) % CONSUMERS) : 0;
-            const int k0 = (g + CONSUMERS - rot) % CONSUMERS;
+            // dynamic (SPO_VDYN, default): every warp takes the run's next group
+            // from the run slot's counter, so a warp delayed on its SMSP (the
+            // producer warp shares SMSP 0's issue slots) takes fewer groups
+            // instead of holding the run back
+            auto take = [&]() -> int {
+                int v = 0;
+                if (lane == 0) v = (int)atomicAdd(&qnext[slot], 1u);
+                return __shfl_sync(0xffffffffu, v, 0);
+            };
+            const int k0 = a.vdyn ? take() : (g + CONSUMERS - rot) % CONSUMERS;
             publish(first_plane(k0 * VM));
             const long long L0 = (long long)it.u * ULANES + lane * W;
             const int nv = (int)max(0LL, min((long long)W, a.lane_limit - L0));
-            for (int q0 = k0 * VM; q0 < it.nb; q0 += CONSUMERS * VM) {
+            for (int q0 = k0 * VM, qn = 0; q0 < it.nb; q0 = qn) {
                 T wx[VM][4], wy[VM][4], wz[VM][4];
                 unsigned s0[VM];
                 int jj[VM];  // windows along j: the position's j-row offset in the plane
@@ -706,7 +756,8 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                             v_plane_done(ax, t00[m], acc[m]);
                         }
                 }
-                publish(first_plane(q0 + CONSUMERS * VM));  // this group's planes are read
+                qn = a.vdyn ? take() * VM : q0 + CONSUMERS * VM;
+                publish(first_plane(qn));  // this group's planes are read
 #pragma unroll
                 for (int m = 0; m < VM; ++m) {
                     if (op[m] < 0) continue;
@@ -724,8 +775,8 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
         return;
     }
     for (int r = 0;; ++r) {
-        const int slot = r & 1;
-        mbar_wait(&rfull[slot], (r >> 1) & 1);
+        const int slot = r % NRS;
+        mbar_wait(&rfull[slot], (r / NRS) & 1);
         const LItem it = info[slot];
         if (!it.valid) break;
         const unsigned char *rc = recs + slot * BPL * RECB;
@@ -806,6 +857,10 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                 }
             }
             if constexpr (!KP && sizeof(T) == 4) finish_z2<KIND>(wz, zs, acc);
+            // (Claiming the next position at the start of this one, to take the
+            // counter / shuffle / record-lookup chain off the gap between two
+            // positions, measured +0.3..1.4% slower for VGH and 5-35% slower for
+            // V groups: scripts/micro/early_ab.sh, profiles/r02/v_dynamic.md.)
             qn = a.dynamic ? take() : q + CONSUMERS;
             publish(first_plane(qn));  // this position's planes are read
             if constexpr (RATIO) {
@@ -833,7 +888,8 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
 
 template <int KIND, typename T, bool RATIO, bool KP, int VGROUP = 1, int WIN = 1>
 static int launch1(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st) {
-    constexpr size_t sm = smem_bytes<T, WIN>();
+    constexpr size_t sm = smem_bytes<T, WIN, rec_slots<KIND, T, VGROUP, WIN>()>();
+    static_assert(sm <= SMEM_BUDGET, "shared memory budget");
     int grid = (int)min((long long)sms, a.n_items);
     if (grid < 1) grid = 1;
     cudaFuncSetAttribute(line_kernel<KIND, T, RATIO, KP, VGROUP, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -854,9 +910,12 @@ static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t 
             if (v == 1) return launch1<KIND, T, RATIO, false, 1, VWIN>(map, a, sms, st);
             if (v == 2) return launch1<KIND, T, RATIO, false, 2, VWIN>(map, a, sms, st);
             if (v == 3) return launch1<KIND, T, RATIO, false, 3, VWIN>(map, a, sms, st);
-            if constexpr (4 * 5 <= ring<T, VWIN>())
+            // group sizes whose planes fit the window ring (ring_min; fp64: up to 3)
+            if constexpr (ring_min(5) <= ring<T, VWIN, rec_slots<KIND, T, 5, VWIN>()>())
                 if (v == 5) return launch1<KIND, T, RATIO, false, 5, VWIN>(map, a, sms, st);
-            return launch1<KIND, T, RATIO, false, 4, VWIN>(map, a, sms, st);
+            if constexpr (ring_min(4) <= ring<T, VWIN, rec_slots<KIND, T, 4, VWIN>()>())
+                return launch1<KIND, T, RATIO, false, 4, VWIN>(map, a, sms, st);
+            return launch1<KIND, T, RATIO, false, 3, VWIN>(map, a, sms, st);
         }
     }
     if constexpr (!KP) {
@@ -876,7 +935,7 @@ static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t 
         if (v == 2) return launch1<KIND, T, RATIO, KP, 2>(map, a, sms, st);
         if (v == 4) return launch1<KIND, T, RATIO, KP, 4>(map, a, sms, st);
         if (v == 3) return launch1<KIND, T, RATIO, KP, 3>(map, a, sms, st);
-        if constexpr (4 * 5 <= LT<T>::R)
+        if constexpr (ring_min(5) <= ring<T, 1, rec_slots<KIND, T, 5, 1>()>())
             if (v == 5) return launch1<KIND, T, RATIO, KP, 5>(map, a, sms, st);
     }
     return launch1<KIND, T, RATIO, KP>(map, a, sms, st);
@@ -1049,6 +1108,13 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     a.dynamic = !(env_dyn && env_dyn[0] == '0');
     const char *env_uni = getenv("SPO_VUNI");
     a.vuni = !(env_uni && env_uni[0] == '0');
+    const char *env_vdyn = getenv("SPO_VDYN");
+    a.vdyn = !(env_vdyn && env_vdyn[0] == '0');
+    // the producer's mbarrier waits spin on try_wait (default); SPO_PSPIN=0:
+    // test_wait + nanosleep back-off, measured 1.6% slower on config 5's V
+    // (profiles/r02/v_dynamic.md)
+    const char *env_pspin = getenv("SPO_PSPIN");
+    a.pspin = !(env_pspin && env_pspin[0] == '0');
     a.dz = g.dinv[2];
     a.dz2 = 2.0 * g.dinv[2] * g.dinv[2];
 
