@@ -665,7 +665,20 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
             const long long L0 = (long long)it.u * ULANES + lane * W;
             const int nv = (int)max(0LL, min((long long)W, a.lane_limit - L0));
             for (int q0 = k0 * VM, qn = 0; q0 < it.nb; q0 = qn) {
-                T wx[VM][4], wy[VM][4], wz[VM][4];
+                // The x weights are used once per plane: read from the record in
+                // shared memory at that point (a broadcast load) instead of held
+                // in 4 (fp64: 8) registers per position: fp32 V -10..12% at 2-4 per
+                // cell, config 5's fp64 V -1..6%.  fp64 reads the y weights the
+                // same way (once per row group; -1..2%; fp32 measured 4-7% slower
+                // with it).  scripts/micro/wx_ab.sh, profiles/r02/v_dynamic.md.
+                constexpr bool WY_SMEM = sizeof(T) == 8;
+                T wy[WY_SMEM ? 1 : VM][4], wz[VM][4];
+                const T *wxp[VM];
+                auto wyj = [&](int m, int j) -> T {  // selects: j is a run-time value on windows
+                    if constexpr (WY_SMEM) return wxp[m][12 + j];
+                    const auto &w = wy[WY_SMEM ? 0 : m];
+                    return j == 0 ? w[0] : (j == 1 ? w[1] : (j == 2 ? w[2] : w[3]));
+                };
                 unsigned s0[VM];
                 int jj[VM];  // windows along j: the position's j-row offset in the plane
                 bool live[VM];
@@ -681,8 +694,8 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                     live[m] = in && cell.x >= 0;
                     op[m] = !in ? -1 : (a.out_index ? a.out_index[cell.w] : cell.w);
                     // the a-rows of x, y, z: weights 0..3, 12..15, 24..27 (k-power: wz[0] = t_z)
-                    load4(rec, wx[m]);
-                    load4(rec + 12 * sizeof(T), wy[m]);
+                    wxp[m] = reinterpret_cast<const T *>(rec);
+                    if constexpr (!WY_SMEM) load4(rec + 12 * sizeof(T), wy[m]);
                     load4(rec + 24 * sizeof(T), wz[m]);
                     s0[m] = base + (unsigned)(cell.z & 0xffff);
                     jj[m] = (cell.y & 0xffff) % win_j(WIN);
@@ -718,10 +731,10 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
 #pragma unroll
                             for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const RV *>(p + (j * 4 + k) * BOXL);
 #pragma unroll
-                            for (int m = 0; m < VM; ++m) v_rowgroup<KP>(c, wz[m], wy[m][j], t00[m]);
+                            for (int m = 0; m < VM; ++m) v_rowgroup<KP>(c, wz[m], wyj(m, j), t00[m]);
                         }
 #pragma unroll
-                        for (int m = 0; m < VM; ++m) v_plane_done(wx[m][i], t00[m], acc[m]);
+                        for (int m = 0; m < VM; ++m) v_plane_done(wxp[m][i], t00[m], acc[m]);
                     }
                     lo = 0xffffffffu;  // done: skip the general loop
                 }
@@ -742,18 +755,14 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                         for (int m = 0; m < VM; ++m) {
                             const int j = WIN == 1 ? r : r - jj[m];
                             if (!(live[m] && x - s0[m] < 4u) || j < 0 || j > 3) continue;
-                            const T wyj = WIN == 1 ? wy[m][r]
-                                                   : (j == 0 ? wy[m][0]
-                                                             : (j == 1 ? wy[m][1] : (j == 2 ? wy[m][2] : wy[m][3])));
-                            v_rowgroup<KP>(c, wz[m], wyj, t00[m]);
+                            v_rowgroup<KP>(c, wz[m], wyj(m, j), t00[m]);
                         }
                     }
 #pragma unroll
                     for (int m = 0; m < VM; ++m)
                         if (live[m] && x - s0[m] < 4u) {
                             const unsigned i = x - s0[m];
-                            const T ax = i == 0 ? wx[m][0] : (i == 1 ? wx[m][1] : (i == 2 ? wx[m][2] : wx[m][3]));
-                            v_plane_done(ax, t00[m], acc[m]);
+                            v_plane_done(wxp[m][i], t00[m], acc[m]);
                         }
                 }
                 qn = a.vdyn ? take() * VM : q0 + CONSUMERS * VM;
@@ -923,15 +932,16 @@ static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t 
     }
     if constexpr (KIND == SPO_KIND_V && !RATIO) {
         // V positions per consumer warp by density (scripts/micro/vm_sweep.py,
-        // profiles/r01/v_groups.jsonl): fp32 2 below 3.5 positions per cell,
-        // else 4; fp64 k-power 4; fp64 B-spline 1 below 4 per cell (its 4 z
-        // weights per position cost registers), else 3 (at 12 consumer warps,
-        // 160 registers, 4 spills: config 5's V 13.1 ms at 3 vs 18.5 at 4,
-        // profiles/r02/f64v_split.md).  SPO_VGROUP=1..5 forces.
+        // profiles/r01/v_groups.jsonl; with dynamic groups and the x weights in
+        // shared memory, profiles/r02/v_dynamic.md): fp32 2 below 3.5 positions
+        // per cell, 3 below 8 (22.7 ms at 4 per cell against 23.2 / 23.3 at 2 /
+        // 4), else 4; fp64 k-power 4; fp64 B-spline 1 below 4 per cell, else 3
+        // (config 5's V 8.9 ms at 3 vs 9.4 at 4).  SPO_VGROUP=1..5 forces.
         const char *e = getenv("SPO_VGROUP");
         const double dens = (double)a.n_pos / (double)a.cells;
         const int v = e ? atoi(e)
-                        : (sizeof(T) == 4 ? (dens < 3.5 ? 2 : 4) : (KP ? 4 : (dens < 4.0 ? 1 : 3)));
+                        : (sizeof(T) == 4 ? (dens < 3.5 ? 2 : (dens < 8.0 ? 3 : 4))
+                                          : (KP ? 4 : (dens < 4.0 ? 1 : 3)));
         if (v == 2) return launch1<KIND, T, RATIO, KP, 2>(map, a, sms, st);
         if (v == 4) return launch1<KIND, T, RATIO, KP, 4>(map, a, sms, st);
         if (v == 3) return launch1<KIND, T, RATIO, KP, 3>(map, a, sms, st);
