@@ -60,6 +60,9 @@ constexpr int BOX = 16 * BOXB;                   // bytes per box (16 rows)
 constexpr int BPL = SPO_LINE_BPL;                // positions per item (run)
 constexpr int PL = 4 * BPL + 4;                  // plane-list ints per run: count, planes, pad
 constexpr int PLB = PL * 4;                      // plane-list bytes per run (16-byte multiple)
+#ifndef SPO_WX_SMEM
+#define SPO_WX_SMEM 0  // 1: every VGL / VGH consumer reads its x weights per slab from shared memory
+#endif
 #ifndef SPO_SPIN_NS
 #define SPO_SPIN_NS 256
 #endif
@@ -855,14 +858,22 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                 const int sl = (int)(x % R);
                 mbar_wait(&full[sl], (x / R) & 1);
                 const T *p = reinterpret_cast<const T *>(planes + (size_t)sl * PB) + corner + lane * W;
+                // fp64 VGH: the x weights of slab i from the record in shared memory
+                // (three broadcast loads per slab) instead of 24 registers: -2.7%,
+                // its spills gone.  fp32 (+0.8%) and fp64 VGL (+0.5%) keep them in
+                // registers (scripts/micro/wxs_ab.sh; -DSPO_WX_SMEM=1 forces all).
+                constexpr bool WXS = SPO_WX_SMEM || (sizeof(T) == 8 && KIND == SPO_KIND_VGH);
+                const T *wr = reinterpret_cast<const T *>(rec);
+                const T ax = WXS ? wr[i] : wx[i], dax = WXS ? wr[4 + i] : wx[4 + i],
+                        d2ax = WXS ? wr[8 + i] : wx[8 + i];
                 if constexpr (KP) {
                     const T dz = (T)a.dz, dz2 = (T)a.dz2;
-                    slab_contract_kp<KIND, BOXL>(p, wy, wz[0], wx[i], wx[4 + i], wx[8 + i], mul_rn(wx[i], dz),
-                                                 mul_rn(wx[4 + i], dz), mul_rn(wx[i], dz2), acc);
+                    slab_contract_kp<KIND, BOXL>(p, wy, wz[0], ax, dax, d2ax, mul_rn(ax, dz), mul_rn(dax, dz),
+                                                 mul_rn(ax, dz2), acc);
                 } else if constexpr (sizeof(T) == 4) {
-                    slab_contract<KIND, BOXL, RJ>(p, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc, zs);
+                    slab_contract<KIND, BOXL, RJ>(p, wy, wz, ax, dax, d2ax, acc, zs);
                 } else {
-                    slab_contract<KIND, BOXL, RJ>(p, wy, wz, wx[i], wx[4 + i], wx[8 + i], acc);
+                    slab_contract<KIND, BOXL, RJ>(p, wy, wz, ax, dax, d2ax, acc);
                 }
             }
             if constexpr (!KP && sizeof(T) == 4) finish_z2<KIND>(wz, zs, acc);
