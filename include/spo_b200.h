@@ -158,12 +158,12 @@ int spo_eval_lanes(int kind, int dtype, int mode, const void *table, const int32
  *   SPO_PATH_TMA      per-position TMA pipeline (spo_eval_tma.cu)
  *   SPO_PATH_LINE     line kernel: 4x4-row planes shared along grid lines
  *                     (j0, k0), for dense batches: VGL/VGH from 4 positions
- *                     per grid cell, V from 3.5 (fp64: 4) (k-power form: 1
+ *                     per grid cell, V from 2.8 (fp64: 4) (k-power form: 1
  *                     and 2) (spo_eval_line.cu)
  *   SPO_PATH_WINDOW   its window variants (B-spline table form): (2+3) x
  *                     (2+3)-row planes shared by the positions of 2 x 2
  *                     (j0, k0) cells, for VGL/VGH from 0.3 positions per cell,
- *                     V from 0.4; for V from 1.5 per cell, (2+3) x 4-row
+ *                     V from 0.4; for V from 1.1 (fp64: 1.3) per cell, (2+3) x 4-row
  *                     planes of two lines along j read once per group of
  *                     positions
  *   SPO_LINE=0/1/2 in the environment forces TMA / line / window.

@@ -389,13 +389,15 @@ extern "C" int64_t spo_eval_workspace_bytes(int kind, int dtype, int mode, int64
 // (j0, k0) cells: +4% at 0.3/cell, +15-20% at 0.5-1/cell over the
 // per-position kernel, +1-5% over the line kernel up to 2.4/cell); the line
 // kernel from LINE_MIN_* (many positions per line: its V position groups
-// and fewer plane loads per slot pay).  V from VWIN_MIN_V per cell to the
+// and fewer plane loads per slot pay).  V from VWIN_MIN_V* per cell to the
 // line kernel: the 2 x 1 window (planes of two lines along j) with V
 // position groups, 7-16% ahead of both the 2 x 2 window and the line kernel
-// there (profiles/r02/v_window.md).  k-power tables: no window variant (rows
+// there (profiles/r02/v_window.md; thresholds re-measured with the dynamic V
+// groups, profiles/r02/v_dynamic.md: fp32 2 x 1 window from 1.1, line from
+// 2.8; fp64 2 x 1 window from 1.3, line from 4).  k-power tables: no window variant (rows
 // have no z halo), the line kernel from 1 (VGL/VGH) / 2 (V) per cell.
-constexpr double WINDOW_MIN_VGX = 0.3, WINDOW_MIN_V = 0.4, VWIN_MIN_V = 1.5;
-constexpr double LINE_MIN_VGX = 4.0, LINE_MIN_V32 = 3.5, LINE_MIN_V64 = 4.0;
+constexpr double WINDOW_MIN_VGX = 0.3, WINDOW_MIN_V = 0.4, VWIN_MIN_V32 = 1.1, VWIN_MIN_V64 = 1.3;
+constexpr double LINE_MIN_VGX = 4.0, LINE_MIN_V32 = 2.8, LINE_MIN_V64 = 4.0;
 constexpr double KP_LINE_MIN_VGX = 1.0, KP_LINE_MIN_V = 2.0;
 
 // Which shared-plane kernel a FAST request takes: 0 = none (the per-position
@@ -407,7 +409,7 @@ static int line_variant(int kind, int dtype, const int32_t *n3, long long n_pos,
     const bool v = kind == SPO_KIND_V;
     auto window = [&]() {
         const char *e = getenv("SPO_VWIN");
-        const bool vw = v && (e ? e[0] == '1' : dens >= VWIN_MIN_V);
+        const bool vw = v && (e ? e[0] == '1' : dens >= (dtype == SPO_F64 ? VWIN_MIN_V64 : VWIN_MIN_V32));
         return vw ? 4 : 3;
     };
     const char *env_line = getenv("SPO_LINE");

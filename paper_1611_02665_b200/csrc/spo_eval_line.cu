@@ -944,14 +944,14 @@ static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t 
     if constexpr (KIND == SPO_KIND_V && !RATIO) {
         // V positions per consumer warp by density (scripts/micro/vm_sweep.py,
         // profiles/r01/v_groups.jsonl; with dynamic groups and the x weights in
-        // shared memory, profiles/r02/v_dynamic.md): fp32 2 below 3.5 positions
-        // per cell, 3 below 8 (22.7 ms at 4 per cell against 23.2 / 23.3 at 2 /
-        // 4), else 4; fp64 k-power 4; fp64 B-spline 1 below 4 per cell, else 3
+        // shared memory, profiles/r02/v_dynamic.md): fp32 3 below 8 positions
+        // per cell (22.7 ms at 4 per cell against 23.2 / 23.3 at 2 / 4; the
+        // line kernel takes V from 2.8 per cell), else 4; fp64 k-power 4; fp64 B-spline 1 below 4 per cell, else 3
         // (config 5's V 8.9 ms at 3 vs 9.4 at 4).  SPO_VGROUP=1..5 forces.
         const char *e = getenv("SPO_VGROUP");
         const double dens = (double)a.n_pos / (double)a.cells;
         const int v = e ? atoi(e)
-                        : (sizeof(T) == 4 ? (dens < 3.5 ? 2 : (dens < 8.0 ? 3 : 4))
+                        : (sizeof(T) == 4 ? (dens < 8.0 ? 3 : 4)
                                           : (KP ? 4 : (dens < 4.0 ? 1 : 3)));
         if (v == 2) return launch1<KIND, T, RATIO, KP, 2>(map, a, sms, st);
         if (v == 4) return launch1<KIND, T, RATIO, KP, 4>(map, a, sms, st);

@@ -110,11 +110,11 @@ def test_eval_path_selection(lib, monkeypatch):
     assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 1048576, big) == 2   # >= 4 positions per cell: line
     assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 262144, big) == 3    # 0.3 .. 4 per cell: window
     assert lib.spo_eval_path(1, 0, 0, n3, 128, 32, 262144, big) == 3    # VGL too
-    assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 1048576, big) == 2   # V from 3.5 per cell: line
-    assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 786432, big) == 3    # V 1.5 .. 3.5: the 2 x 1 window
+    assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 786432, big) == 2    # V from 2.8 per cell: line
+    assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 655360, big) == 3    # V 1.1 .. 2.8: the 2 x 1 window
     assert lib.spo_eval_path(0, 1, 0, n3, 64, 64, 983040, big) == 3     # fp64 V below 4 per cell: window
     assert lib.spo_eval_path(0, 1, 0, n3, 64, 64, 1048576, big) == 2    # fp64 V from 4: line
-    assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 262144, big) == 3    # V 0.4 .. 1.5 per cell: 2 x 2 window
+    assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 262144, big) == 3    # V 0.4 .. 1.1 per cell: 2 x 2 window
     assert lib.spo_eval_path(0, 0, 0, n3, 128, 32, 78643, big) == 1     # V below 0.3 per cell: TMA
     assert lib.spo_eval_path(2, 0, 0, n3, 128, 32, 60000, big) == 1     # sparser: per-position TMA
     assert lib.spo_eval_path(2, 0, 1, n3, 128, 32, 262144, big) == 0    # strict: generic
