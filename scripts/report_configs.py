@@ -169,7 +169,8 @@ def phase_md(args):
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         peak = float(json.load(f)["hbm_gbs"])
     rows = [json.loads(x) for x in open(args.time)]
-    ncu = ncu_rows(args.ncu) if args.ncu else []
+    # --ncu: an .ncu-rep, or the rows already extracted from one on the GPU box (.json)
+    ncu = (json.load(open(args.ncu)) if args.ncu.endswith(".json") else ncu_rows(args.ncu)) if args.ncu else []
     cpu = {}
     if args.cpu:
         for ln in open(args.cpu):
@@ -198,7 +199,25 @@ def phase_md(args):
             f"{'%.1f' % pipe if pipe is not None else '—'} | "
             f"{r['max_err_over_tol_scale']:.3f} ({r['oracle_positions']}) | "
             f"{cpu_s} |")
-    text = "\n".join(lines) + "\n"
+    # the BASELINE.md section 4 columns
+    base = [f"| cfg | kernel | GPUs | orbital-evals/s | algorithmic GB/s | fraction of {peak:.1f} GB/s "
+            "(irreducible-bytes fraction) | ncu DRAM GB/s | L2 hit % | max err / Σ\\|w·c\\| | "
+            "CPU ref orbital-evals/s (cores) |", "|---|---|---|---|---|---|---|---|---|---|"]
+    for i, r in enumerate(rows):
+        n = ncu[i] if i < len(ncu) else {}
+        n = n if n and n.get("dram_read") == n.get("dram_read") else {}
+        dram = (n["dram_read"] + n["dram_write"]) / (n["ms"] * 1e-3) / 1e9 if n else None
+        c = cpu.get((r["config"], r["kind"]))
+        cpu_s = (f"{c['all_threads']:.2e} ({c['threads']})" + (" fp32 kernels" if r["dtype"] == "f64" else "")) \
+            if c else "—"
+        base.append(
+            f"| {r['config']} | {r['kind'].upper()} ({r['path']} kernel, {r['dtype']}, N={r['n_splines']}) | 1 | "
+            f"{r['orbital_evals_per_s']:.3e} | {r['algorithmic_gbs']:,.0f} | {r['fraction']:.2f} "
+            f"({r['frac_irreducible']:.2f}) | {'%.0f' % dram if dram else '—'} | "
+            f"{'%.1f' % n['l2_hit'] if n else '—'} | {r['max_err_over_tol_scale'] * r['tol']:.1e} "
+            f"(tol {r['tol']:.0e}; {r['oracle_positions']} oracle positions) | {cpu_s} |")
+    text = ("## BASELINE.md section 4 columns\n\n" + "\n".join(base) + "\n\n## Extended\n\n"
+            + "\n".join(lines) + "\n")
     if args.md:
         with open(args.md, "w") as f:
             f.write(text)

@@ -170,3 +170,39 @@ def test_line_edge_coordinates(monkeypatch):
     pos = np.stack([rng.choice(xs, 20000), rng.choice(xs, 20000), rng.random(20000)], axis=1)
     a, b = _both(monkeypatch, dt, "vgh", pos)
     assert _eq(a, b)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_v_group_sizes_and_assignment(monkeypatch, dtype):
+    """Every V group size the launcher accepts (SPO_VGROUP, including the ones
+    the ring cannot hold, which fall back), on the line kernel and the 2 x 1
+    window, with the groups handed out dynamically (default) and statically
+    (SPO_VDYN=0), the same-cell path on and off: bitwise equal to the
+    per-position kernel.  The timeout is the deadlock check (a ring smaller
+    than 4 VGROUP + PBATCH - 1 planes would hang; ring_min in the kernel)."""
+    grid = unit_cell_grid(12)
+    dt = DeviceTable.random(grid, 256, seed=3) if dtype == "f32" else DeviceTable.normal_f64(grid, 128, seed=3)
+    rng = np.random.default_rng(8)
+    dense = rng.random((12 ** 3 * 9 + 5, 3))  # ~9 per cell: same-cell groups and mixed ones
+    dense[rng.integers(0, len(dense), size=4)] = np.nan
+    import torch
+
+    dense = torch.from_numpy(dense).cuda()  # device input: non-finite positions go through the status flag
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    kw = dict(pipeline=True, status=st, check=False)
+    monkeypatch.setenv("SPO_LINE", "0")
+    ref = evaluate(dt, "v", dense, **kw).clone()
+    for line, vwin in (("1", None), ("2", "1")):
+        monkeypatch.setenv("SPO_LINE", line)
+        if vwin:
+            monkeypatch.setenv("SPO_VWIN", vwin)
+        for vg in ("1", "2", "3", "4", "5"):
+            monkeypatch.setenv("SPO_VGROUP", vg)
+            for knobs in ({}, {"SPO_VDYN": "0"}, {"SPO_VUNI": "0"}, {"SPO_PSPIN": "0"}):
+                for k, v in knobs.items():
+                    monkeypatch.setenv(k, v)
+                got = evaluate(dt, "v", dense, **kw)
+                assert _eq(got, ref), (line, vwin, vg, knobs)
+                for k in knobs:
+                    monkeypatch.delenv(k)
