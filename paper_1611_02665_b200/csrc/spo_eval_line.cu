@@ -155,6 +155,8 @@ struct LArgs {
     int dynamic;                // consumers take positions from a shared per-run counter
     int vuni;                   // V groups: the unrolled same-cell path (SPO_VUNI=0 disables, for A/B)
     int pspin;                  // producer mbarrier waits: 1 = tight try_wait spin, 0 = test + nanosleep back-off
+    int vgroup;                 // V positions per consumer warp (the group kernels' VGROUP)
+    int cellgroups;             // V groups aligned to cells by line_runs_kernel (group starts in the records)
     int vdyn;                   // V groups taken from a shared per-run counter (SPO_VDYN=0: rotated static)
     long long cells;            // grid cells (positions per cell pick the V group size)
 };
@@ -268,8 +270,9 @@ __global__ void line_records_kernel(GridArgs g, const double *__restrict__ pos, 
 constexpr int RUNS_PER_BLOCK = 4;
 template <typename T>
 __global__ void __launch_bounds__(32 * RUNS_PER_BLOCK)
-    line_runs_kernel(long long n, unsigned char *__restrict__ recs, int *__restrict__ plist, int win) {
+    line_runs_kernel(long long n, unsigned char *__restrict__ recs, int *__restrict__ plist, int win, int vgroup) {
     static_assert(BPL == 64, "two positions per lane");
+    __shared__ unsigned char gs_all[RUNS_PER_BLOCK][BPL];  // vgroup > 0: start position of the run's group k
     constexpr int RECB = LT<T>::RECB;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long b = blockIdx.x * (long long)RUNS_PER_BLOCK + w;
@@ -277,7 +280,8 @@ __global__ void __launch_bounds__(32 * RUNS_PER_BLOCK)
     const int nb = (int)min((long long)BPL, n - b * BPL);
     unsigned char *rc = recs + b * BPL * RECB + 36 * sizeof(T);
     int *pl = plist + b * PL;
-    int i0[2], wj[2], wk[2];
+    unsigned char *gs = gs_all[w];
+    int i0[2], wj[2], wk[2], cy[2];
     bool ok[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -286,6 +290,8 @@ __global__ void __launch_bounds__(32 * RUNS_PER_BLOCK)
         if (q < nb) c = *reinterpret_cast<const int4 *>(rc + q * RECB);
         ok[e] = c.x >= 0;
         i0[e] = c.x;
+        cy[e] = c.y;
+        gs[q] = 0xff;
         const int j0 = c.y & 0xffff, k0 = c.y >> 16;
         wj[e] = win_j(win) * (j0 / win_j(win));
         wk[e] = win_k(win) * (k0 / win_k(win));
@@ -318,7 +324,7 @@ __global__ void __launch_bounds__(32 * RUNS_PER_BLOCK)
                     cj = aj;
                     ck = ak;
                 }
-                c->z = s;
+                c->z = s | (vgroup > 0 && q > 0 ? q << 16 : 0);  // cell groups: every position its own group
             }
             reinterpret_cast<int4 *>(rc)->z |= next << 16;
             pl[0] = next;
@@ -369,6 +375,40 @@ __global__ void __launch_bounds__(32 * RUNS_PER_BLOCK)
         if (lane >= d) incl += o;
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (vgroup > 0) {
+        // Cell-aligned V groups: a group starts at every new cell (a non-finite
+        // position is a cell of its own) and after every vgroup positions of a
+        // cell.  Position-in-cell = q - (start of q's cell), the start by a max
+        // scan over the new-cell positions; the group number is the prefix sum
+        // of the group-start flags; gs[k] = first position of group k.
+        const int pi = __shfl_up_sync(0xffffffffu, i0[1], 1), py = __shfl_up_sync(0xffffffffu, cy[1], 1);
+        bool nc[2];
+        nc[0] = lane == 0 || !ok[0] || i0[0] != pi || cy[0] != py;
+        nc[1] = !ok[1] || i0[1] != i0[0] || cy[1] != cy[0];
+        int cs = nc[1] ? 2 * lane + 1 : (nc[0] ? 2 * lane : -1);  // last cell start in this lane
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, cs, d);
+            if (lane >= d) cs = max(cs, o);
+        }
+        const int csb = __shfl_up_sync(0xffffffffu, cs, 1);  // last cell start before this lane
+        const int st0 = nc[0] ? 2 * lane : csb;
+        const int st1 = nc[1] ? 2 * lane + 1 : st0;
+        bool gf[2];
+        gf[0] = 2 * lane < nb && (2 * lane - st0) % vgroup == 0;
+        gf[1] = 2 * lane + 1 < nb && (2 * lane + 1 - st1) % vgroup == 0;
+        int gi = (int)gf[0] + (int)gf[1];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, gi, d);
+            if (lane >= d) gi += o;
+        }
+        const int g1 = gi - 1, g0 = g1 - (int)gf[1];  // group numbers of the lane's two positions
+        __syncwarp();
+        if (gf[0]) gs[g0] = (unsigned char)(2 * lane);
+        if (gf[1]) gs[g1] = (unsigned char)(2 * lane + 1);
+        __syncwarp();
+    }
     int next = incl - cnt[0] - cnt[1];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -378,7 +418,9 @@ __global__ void __launch_bounds__(32 * RUNS_PER_BLOCK)
             s = (same[e] && i0[e] <= lastp[e]) ? next - 1 - (lastp[e] - i0[e]) : next;
             for (int t = 0; t < cnt[e]; ++t) pl[1 + next + t] = (lo[e] + t) | (wj[e] << 10) | (wk[e] << 20);
         }
-        if (q < nb) reinterpret_cast<int4 *>(rc + q * RECB)->z = s | (q == 0 ? total << 16 : 0);
+        if (q < nb)
+            reinterpret_cast<int4 *>(rc + q * RECB)->z =
+                s | (q == 0 ? total << 16 : (vgroup > 0 ? (int)gs[q] << 16 : 0));
         next += cnt[e];
     }
     if (lane == 0) pl[0] = total;
@@ -440,6 +482,17 @@ constexpr int WIN_CELLS = SPO_WIN_CELLS;  // window side (cells) of the window v
 // position groups read a plane once for several positions with no k offset
 // to select (win_k = 1)
 constexpr int VWIN = 21;
+// V groups aligned to cells from this many positions per cell (below, most
+// same-cell runs are shorter than a group and the general path's plane sharing
+// between neighbouring cells is worth more).  Measured with groups of 3
+// (profiles/r02/v_cell_groups.md): fp64 -3.4% at 4.7 per cell, -4% at 7.1, -5% at
+// 16.3 (config 5's V); fp32 +1% at 4, 0 at 6, -3% at 8 per cell.
+#ifndef SPO_CELL_GROUPS_MIN32
+#define SPO_CELL_GROUPS_MIN32 7.0
+#endif
+#ifndef SPO_CELL_GROUPS_MIN64
+#define SPO_CELL_GROUPS_MIN64 4.5
+#endif
 static_assert(smem_bytes<float>() <= SMEM_BUDGET, "shared memory budget");
 static_assert(smem_bytes<double>() <= SMEM_BUDGET, "shared memory budget");
 static_assert(smem_bytes<float, WIN_CELLS>() <= SMEM_BUDGET, "shared memory budget");
@@ -663,11 +716,26 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                 if (lane == 0) v = (int)atomicAdd(&qnext[slot], 1u);
                 return __shfl_sync(0xffffffffu, v, 0);
             };
-            const int k0 = a.vdyn ? take() : (g + CONSUMERS - rot) % CONSUMERS;
-            publish(first_plane(k0 * VM));
+            // Groups: fixed (group k = positions k VM .. k VM + VM - 1 of the run),
+            // or, on dense batches, aligned to cells by line_runs_kernel
+            // (a.cellgroups): group k starts at the position stored in record k
+            // (bits 16..23 of cell.z; 0xff: no such group) and holds up to VM
+            // positions of ONE cell, so every group takes the unrolled same-cell
+            // path below.
+            auto gstart = [&](int k) -> int {
+                if (k >= it.nb) return it.nb;
+                if (k == 0) return 0;
+                const int v = (reinterpret_cast<const int4 *>(rc + k * RECB + 36 * sizeof(T))->z >> 16) & 0xff;
+                return v == 0xff ? it.nb : v;
+            };
+            auto qof = [&](int k) -> int { return a.cellgroups ? gstart(k) : k * VM; };
+            int kcur = a.vdyn ? take() : (g + CONSUMERS - rot) % CONSUMERS;
+            int q0 = qof(kcur);
+            publish(first_plane(q0));
             const long long L0 = (long long)it.u * ULANES + lane * W;
             const int nv = (int)max(0LL, min((long long)W, a.lane_limit - L0));
-            for (int q0 = k0 * VM, qn = 0; q0 < it.nb; q0 = qn) {
+            while (q0 < it.nb) {
+                const int ng = a.cellgroups ? gstart(kcur + 1) - q0 : VM;  // positions of this group
                 // The x weights are used once per plane: read from the record in
                 // shared memory at that point (a broadcast load) instead of held
                 // in 4 (fp64: 8) registers per position: fp32 V -10..12% at 2-4 per
@@ -691,7 +759,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                 unsigned lo = 0xffffffffu, hi = 0;
 #pragma unroll
                 for (int m = 0; m < VM; ++m) {
-                    const bool in = q0 + m < it.nb;
+                    const bool in = m < ng && q0 + m < it.nb;
                     const unsigned char *rec = rc + min(q0 + m, it.nb - 1) * RECB;
                     const int4 cell = *reinterpret_cast<const int4 *>(rec + 36 * sizeof(T));
                     live[m] = in && cell.x >= 0;
@@ -716,10 +784,9 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                 // tests (the general loop below spends ~60% of its instructions on
                 // them: ncu on config 5's V, profiles/r02/f64v_uniform.md).  Each
                 // position sees exactly the general loop's sequence (bitwise).
-                bool uni = a.vuni && live[0];
-#pragma unroll
-                for (int m = 1; m < VM; ++m) uni = uni && live[m] && s0[m] == s0[0] && (WIN == 1 || jj[m] == jj[0]);
-                if (uni) {
+                // the first NN positions of the group on the same four planes
+                auto same_cell = [&](auto nn) {
+                    constexpr int NN = decltype(nn)::value;
                     await_issued(hi);  // planes are armed in order: lo .. hi are all issued
                     const int roff = WIN == 1 ? 0 : jj[0] * 4 * BOXL;
 #pragma unroll
@@ -734,12 +801,31 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
 #pragma unroll
                             for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const RV *>(p + (j * 4 + k) * BOXL);
 #pragma unroll
-                            for (int m = 0; m < VM; ++m) v_rowgroup<KP>(c, wz[m], wyj(m, j), t00[m]);
+                            for (int m = 0; m < NN; ++m) v_rowgroup<KP>(c, wz[m], wyj(m, j), t00[m]);
                         }
 #pragma unroll
-                        for (int m = 0; m < VM; ++m) v_plane_done(wxp[m][i], t00[m], acc[m]);
+                        for (int m = 0; m < NN; ++m) v_plane_done(wxp[m][i], t00[m], acc[m]);
+                    }
+                };
+                if (a.cellgroups) {
+                    // 1 .. VM positions of one cell (a non-finite position is a group of its own)
+                    if (live[0]) {
+                        if (ng >= VM) same_cell(std::integral_constant<int, VM>{});
+                        else if (ng == 1) same_cell(std::integral_constant<int, 1>{});
+                        else if (ng == 2) same_cell(std::integral_constant<int, (VM > 2 ? 2 : 1)>{});
+                        else if (ng == 3) same_cell(std::integral_constant<int, (VM > 3 ? 3 : 1)>{});
+                        else same_cell(std::integral_constant<int, (VM > 4 ? 4 : 1)>{});
                     }
                     lo = 0xffffffffu;  // done: skip the general loop
+                } else {
+                    bool uni = a.vuni && live[0];
+#pragma unroll
+                    for (int m = 1; m < VM; ++m)
+                        uni = uni && live[m] && s0[m] == s0[0] && (WIN == 1 || jj[m] == jj[0]);
+                    if (uni) {
+                        same_cell(std::integral_constant<int, VM>{});
+                        lo = 0xffffffffu;  // done: skip the general loop
+                    }
                 }
                 for (unsigned x = lo; lo != 0xffffffffu && x <= hi; ++x) {
                     await_issued(x);
@@ -768,7 +854,8 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                             v_plane_done(wxp[m][i], t00[m], acc[m]);
                         }
                 }
-                qn = a.vdyn ? take() * VM : q0 + CONSUMERS * VM;
+                kcur = a.vdyn ? take() : kcur + CONSUMERS;
+                const int qn = qof(kcur);
                 publish(first_plane(qn));  // this group's planes are read
 #pragma unroll
                 for (int m = 0; m < VM; ++m) {
@@ -779,6 +866,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                     else if (nv > 0)
                         store_lane_partial<1>(o, a.out_stream_stride, acc[m], live[m], nv);
                 }
+                q0 = qn;
             }
             base += count;
             __syncwarp();
@@ -917,16 +1005,49 @@ static int launch1(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t
     line_kernel<KIND, T, RATIO, KP, VGROUP, WIN><<<grid, threads<T, KP>(), sm, st>>>(map, a);
     return check_launch("spo_eval (line) launch");
 }
+// V positions per consumer warp (the VGROUP the V launch is instantiated with;
+// chosen before the prologue, which aligns the groups to cells on dense
+// batches).  SPO_VGROUP=1..5 forces; sizes the plane ring cannot hold
+// (ring_min) fall back to the next smaller one.
+//  * 2 x 1 windows (profiles/r02/v_window.md): fp32 2 below 1.75 positions per
+//    cell, else 4; fp64 3.
+//  * lines (scripts/micro/vm_sweep.py, profiles/r01/v_groups.jsonl; with dynamic
+//    groups and the x weights in shared memory, profiles/r02/v_dynamic.md): fp32
+//    3 below 8 per cell (22.7 ms at 4 per cell against 23.2 / 23.3 at 2 / 4),
+//    else 4; fp64 k-power 4; fp64 B-spline 1 below 4 per cell, else 3; with
+//    cell-aligned groups (cell): 3 (groups of 4 and 5 aligned to cells measured
+//    8-70% slower than fixed ones, profiles/r02/v_cell_groups.md).
+#ifndef SPO_CELL_VGROUP32
+#define SPO_CELL_VGROUP32 3
+#endif
+#ifndef SPO_CELL_VGROUP64
+#define SPO_CELL_VGROUP64 3
+#endif
+template <typename T>
+static int v_group_size(bool kp, int win, double dens, bool cell) {
+    const char *e = getenv("SPO_VGROUP");
+    if (!kp && win > 1 && win != VWIN) return 1;  // the 2 x 2 window: no groups
+    int v;
+    if (!kp && win == VWIN) {
+        v = e ? atoi(e) : (sizeof(T) == 4 ? (dens < 1.75 ? 2 : 4) : 3);
+        v = v < 1 ? 1 : (v > 5 ? 5 : v);
+        if (v == 5 && !(ring_min(5) <= ring<T, VWIN, rec_slots<SPO_KIND_V, T, 5, VWIN>()>())) v = 4;
+        if (v == 4 && !(ring_min(4) <= ring<T, VWIN, rec_slots<SPO_KIND_V, T, 4, VWIN>()>())) v = 3;
+        return v;
+    }
+    v = e ? atoi(e)
+          : (cell ? (sizeof(T) == 4 ? SPO_CELL_VGROUP32 : SPO_CELL_VGROUP64)
+                  : (sizeof(T) == 4 ? (dens < 8.0 ? 3 : 4) : (kp ? 4 : (dens < 4.0 ? 1 : 3))));
+    v = v < 1 ? 1 : (v > 5 ? 5 : v);
+    if (v == 5 && !(ring_min(5) <= ring<T, 1, rec_slots<SPO_KIND_V, T, 5, 1>()>())) v = 4;
+    return v;
+}
+
 template <int KIND, typename T, bool RATIO, bool KP>
 static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t st, int win) {
     if constexpr (!KP && KIND == SPO_KIND_V && !RATIO) {
         if (win == VWIN) {
-            // V groups on 2 x 1 windows (profiles/r02/v_window.md): fp32 2
-            // positions per warp below 1.75 per cell, else 4; fp64 3.
-            // SPO_VGROUP=1..5 forces.
-            const char *e = getenv("SPO_VGROUP");
-            const double dens = (double)a.n_pos / (double)a.cells;
-            const int v = e ? atoi(e) : (sizeof(T) == 4 ? (dens < 1.75 ? 2 : 4) : 3);
+            const int v = a.vgroup;  // v_group_size(): a size this ring holds
             if (v == 1) return launch1<KIND, T, RATIO, false, 1, VWIN>(map, a, sms, st);
             if (v == 2) return launch1<KIND, T, RATIO, false, 2, VWIN>(map, a, sms, st);
             if (v == 3) return launch1<KIND, T, RATIO, false, 3, VWIN>(map, a, sms, st);
@@ -942,17 +1063,7 @@ static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t 
         if (win > 1) return launch1<KIND, T, RATIO, false, 1, WIN_CELLS>(map, a, sms, st);
     }
     if constexpr (KIND == SPO_KIND_V && !RATIO) {
-        // V positions per consumer warp by density (scripts/micro/vm_sweep.py,
-        // profiles/r01/v_groups.jsonl; with dynamic groups and the x weights in
-        // shared memory, profiles/r02/v_dynamic.md): fp32 3 below 8 positions
-        // per cell (22.7 ms at 4 per cell against 23.2 / 23.3 at 2 / 4; the
-        // line kernel takes V from 2.8 per cell), else 4; fp64 k-power 4; fp64 B-spline 1 below 4 per cell, else 3
-        // (config 5's V 8.9 ms at 3 vs 9.4 at 4).  SPO_VGROUP=1..5 forces.
-        const char *e = getenv("SPO_VGROUP");
-        const double dens = (double)a.n_pos / (double)a.cells;
-        const int v = e ? atoi(e)
-                        : (sizeof(T) == 4 ? (dens < 8.0 ? 3 : 4)
-                                          : (KP ? 4 : (dens < 4.0 ? 1 : 3)));
+        const int v = a.vgroup;  // v_group_size()
         if (v == 2) return launch1<KIND, T, RATIO, KP, 2>(map, a, sms, st);
         if (v == 4) return launch1<KIND, T, RATIO, KP, 4>(map, a, sms, st);
         if (v == 3) return launch1<KIND, T, RATIO, KP, 3>(map, a, sms, st);
@@ -1087,13 +1198,25 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     if (cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, vals, (int)n_pos, 0, key_bits, st) != cudaSuccess)
         return check_launch("spo_eval (line sort)");
     const int *order = vals.Current();  // the sorted original indices (either buffer)
+    // V groups: size, and whether line_runs_kernel aligns them to cells (dense
+    // batches: most groups then sit in one cell; SPO_VCELL=0/1 forces)
+    const bool kpower = geo.kmul != 1;
+    const double dens = (double)n_pos / ((double)geo.nx * geo.ny * geo.nz);
+    int vgroup = 1, cellgroups = 0;
+    if (kind == SPO_KIND_V && !ratio) {
+        const char *env_cell = getenv("SPO_VCELL");
+        const bool cell = env_cell ? env_cell[0] == '1' : dens >= (dtype == SPO_F64 ? SPO_CELL_GROUPS_MIN64 : SPO_CELL_GROUPS_MIN32);
+        vgroup = dtype == SPO_F64 ? v_group_size<double>(kpower, win, dens, cell)
+                                  : v_group_size<float>(kpower, win, dens, cell);
+        cellgroups = cell && vgroup > 1 ? vgroup : 0;
+    }
     const unsigned run_blocks = (unsigned)((n_pos + (long long)BPL * RUNS_PER_BLOCK - 1) / ((long long)BPL * RUNS_PER_BLOCK));
     if (dtype == SPO_F64) {
         line_records_kernel<double><<<pg.blocks, pg.threads, 0, st>>>(g, pos, order, n_pos, recs, geo.kmul != 1);
-        line_runs_kernel<double><<<run_blocks, 32 * RUNS_PER_BLOCK, 0, st>>>(n_pos, recs, plist, win);
+        line_runs_kernel<double><<<run_blocks, 32 * RUNS_PER_BLOCK, 0, st>>>(n_pos, recs, plist, win, cellgroups);
     } else {
         line_records_kernel<float><<<pg.blocks, pg.threads, 0, st>>>(g, pos, order, n_pos, recs, geo.kmul != 1);
-        line_runs_kernel<float><<<run_blocks, 32 * RUNS_PER_BLOCK, 0, st>>>(n_pos, recs, plist, win);
+        line_runs_kernel<float><<<run_blocks, 32 * RUNS_PER_BLOCK, 0, st>>>(n_pos, recs, plist, win, cellgroups);
     }
     int rc = check_launch("spo_eval (line prologue)");
     if (rc) return rc;
@@ -1129,6 +1252,8 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     a.dynamic = !(env_dyn && env_dyn[0] == '0');
     const char *env_uni = getenv("SPO_VUNI");
     a.vuni = !(env_uni && env_uni[0] == '0');
+    a.vgroup = vgroup;
+    a.cellgroups = cellgroups;
     const char *env_vdyn = getenv("SPO_VDYN");
     a.vdyn = !(env_vdyn && env_vdyn[0] == '0');
     // the producer's mbarrier waits spin on try_wait (default); SPO_PSPIN=0:

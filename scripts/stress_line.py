@@ -41,6 +41,9 @@ def main():
         kind = ["v", "vgl", "vgh"][int(rng.integers(0, 3))]
         dens = float(rng.choice([0.05, 0.15, 0.3, 0.8, 1.5, 3.0, 6.0, 17.0]))
         P = max(1, int(dens * np.prod(n3))) + int(rng.integers(0, 64))
+        # three full outputs are alive at once: keep each under 8 GB
+        S = {"v": 1, "vgl": 5, "vgh": 10}[kind]
+        P = min(P, int(8e9 / (S * (n + q) * (8 if f64 else 4))))
         pos = rng.random((P, 3)) * 3.0 - 1.0
         if rng.random() < 0.2:
             pos[rng.integers(0, P, size=3), rng.integers(0, 3, size=3)] = np.nan
@@ -51,13 +54,13 @@ def main():
             st = torch.zeros(1, dtype=torch.int32, device="cuda")
             outs.append(evaluate(dt, kind, dpos, pipeline=True, form=form, status=st, check=False))
         torch.cuda.synchronize()
-        a, w, b = (o.nan_to_num(123.0) for o in outs)
-        ok = bool(torch.equal(a, b)) and bool(torch.equal(w, b))
+        b = outs[2].nan_to_num(123.0)
+        ok = all(bool(torch.equal(o.nan_to_num(123.0), b)) for o in outs[:2])
         print(f"{it:3d} grid={n3} N={n} {'f64' if f64 else 'f32'} tile={tile} {form} {kind} P={P} "
               f"({dens}/cell) {'ok' if ok else 'MISMATCH'}", flush=True)
         if not ok:
             return 1
-        del dt, outs, a, w, b
+        del dt, outs, b
         torch.cuda.empty_cache()
     print(f"all {iters} cases bitwise equal ({time.time() - t0:.0f} s)")
     return 0

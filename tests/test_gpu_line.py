@@ -178,8 +178,8 @@ def test_v_group_sizes_and_assignment(monkeypatch, dtype):
     """Every V group size the launcher accepts (SPO_VGROUP, including the ones
     the ring cannot hold, which fall back), on the line kernel and the 2 x 1
     window, with the groups handed out dynamically (default) and statically
-    (SPO_VDYN=0), the same-cell path on and off: bitwise equal to the
-    per-position kernel.  The timeout is the deadlock check (a ring smaller
+    (SPO_VDYN=0), the same-cell path on and off, the groups fixed or aligned to
+    cells by the prologue (SPO_VCELL): bitwise equal to the per-position kernel.  The timeout is the deadlock check (a ring smaller
     than 4 VGROUP + PBATCH - 1 planes would hang; ring_min in the kernel)."""
     grid = unit_cell_grid(12)
     dt = DeviceTable.random(grid, 256, seed=3) if dtype == "f32" else DeviceTable.normal_f64(grid, 128, seed=3)
@@ -199,7 +199,8 @@ def test_v_group_sizes_and_assignment(monkeypatch, dtype):
             monkeypatch.setenv("SPO_VWIN", vwin)
         for vg in ("1", "2", "3", "4", "5"):
             monkeypatch.setenv("SPO_VGROUP", vg)
-            for knobs in ({}, {"SPO_VDYN": "0"}, {"SPO_VUNI": "0"}, {"SPO_PSPIN": "0"}):
+            for knobs in ({}, {"SPO_VDYN": "0"}, {"SPO_VUNI": "0"}, {"SPO_PSPIN": "0"}, {"SPO_VCELL": "0"},
+                          {"SPO_VCELL": "1"}, {"SPO_VCELL": "1", "SPO_VDYN": "0"}):
                 for k, v in knobs.items():
                     monkeypatch.setenv(k, v)
                 got = evaluate(dt, "v", dense, **kw)
