@@ -487,9 +487,6 @@ constexpr int VWIN = 21;
 // between neighbouring cells is worth more).  Measured with groups of 3
 // (profiles/r02/v_cell_groups.md): fp64 -3.4% at 4.7 per cell, -4% at 7.1, -5% at
 // 16.3 (config 5's V); fp32 +1% at 4, 0 at 6, -3% at 8 per cell.
-#ifndef SPO_CELL_RT
-#define SPO_CELL_RT 0
-#endif
 #ifndef SPO_CELL_GROUPS_MIN32
 #define SPO_CELL_GROUPS_MIN32 7.0
 #endif
@@ -812,33 +809,6 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                 };
                 if (a.cellgroups) {
                     // 1 .. VM positions of one cell (a non-finite position is a group of its own)
-#if SPO_CELL_RT
-                    // one body, the group's size tested per position (warp-uniform
-                    // branches) instead of one unrolled body per size
-                    if (live[0]) {
-                        await_issued(hi);
-                        const int roff = WIN == 1 ? 0 : jj[0] * 4 * BOXL;
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const unsigned x = lo + (unsigned)i;
-                            const int sl = (int)(x % R);
-                            mbar_wait(&full[sl], (x / R) & 1);
-                            const T *p = reinterpret_cast<const T *>(planes + (size_t)sl * PB) + roff + lane * W;
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                RV c[4];
-#pragma unroll
-                                for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const RV *>(p + (j * 4 + k) * BOXL);
-#pragma unroll
-                                for (int m = 0; m < VM; ++m)
-                                    if (m < ng) v_rowgroup<KP>(c, wz[m], wyj(m, j), t00[m]);
-                            }
-#pragma unroll
-                            for (int m = 0; m < VM; ++m)
-                                if (m < ng) v_plane_done(wxp[m][i], t00[m], acc[m]);
-                        }
-                    }
-#else
                     if (live[0]) {
                         if (ng >= VM) same_cell(std::integral_constant<int, VM>{});
                         else if (ng == 1) same_cell(std::integral_constant<int, 1>{});
@@ -846,7 +816,6 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                         else if (ng == 3) same_cell(std::integral_constant<int, (VM > 3 ? 3 : 1)>{});
                         else same_cell(std::integral_constant<int, (VM > 4 ? 4 : 1)>{});
                     }
-#endif
                     lo = 0xffffffffu;  // done: skip the general loop
                 } else {
                     bool uni = a.vuni && live[0];

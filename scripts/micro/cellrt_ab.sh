@@ -1,3 +1,4 @@
+# record: the SPO_CELL_RT variant lived in commit be5f965 only (removed after this A/B, profiles/r02/v_cell_groups.md)
 # aligned V groups: one unrolled body per group size (default build) against one body with
 # the size tested per position (-DSPO_CELL_RT=1, libspo_b200_cellrt.so), group sizes swept;
 # SPO_VCELL=0 (fixed groups) rides along as the reference and the bitwise check
