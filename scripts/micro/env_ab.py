@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--envs", required=True, help="';'-separated variants, each ','-separated K=V pairs")
     ap.add_argument("--cases", default=DEFAULT)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--form", default="auto", help="table form: auto (B-spline) or kpower (opt-in)")
     args = ap.parse_args()
     variants = [dict(kv.split("=") for kv in v.split(",") if kv) for v in args.envs.split(";")]
     keys = sorted({k for v in variants for k in v})
@@ -53,6 +54,8 @@ def main():
             tables[cfg.index] = (DeviceTable.normal_f64(cfg.grid, 512 if cfg.index == 5 else cfg.n_splines, seed=0)
                                  if cfg.dtype == "f64" else DeviceTable.random(cfg.grid, cfg.n_splines, seed=0))
         dt = tables[cfg.index]
+        if args.form == "kpower":
+            dt.with_kpower()
         P = pos.shape[0]
         S = {"v": 1, "vgl": 5, "vgh": 10}[kind]
         out = torch.empty((P, S, dt.lanes), dtype=dt.data.dtype, device="cuda")
@@ -64,7 +67,7 @@ def main():
                 for k in keys:
                     os.environ.pop(k, None)
                 os.environ.update(v)
-                t = timed(lambda: evaluate(dt, kind, pos, out, pipeline=True, check=False), args.reps)
+                t = timed(lambda: evaluate(dt, kind, pos, out, pipeline=True, check=False, form=args.form), args.reps)
                 label = ",".join(f"{k}={x}" for k, x in v.items()) or "default"
                 res[label] = round(min(res.get(label, 1e9), t * 1e3), 4)
                 if rnd == 0:
