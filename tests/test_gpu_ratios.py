@@ -131,3 +131,27 @@ def test_ratios_against_oracle(torch, monkeypatch, kind, dtype, line):
     bound = tol * np.einsum("psn,pn->ps", scale, np.abs(c))
     err = np.abs(got[sel] - want)
     assert (err <= bound).all(), float((err / bound).max())
+
+
+@pytest.mark.parametrize("kind", ["v", "vgh"])
+def test_orbital_sharded_ratios_sum_to_the_full_table(torch, kind):
+    """multi.evaluate_ratios_orbital_sharded, the slices of a 3-way orbital
+    partition evaluated one after the other on this GPU (world 1: the reduce is
+    the identity): the partials add up to evaluate_ratios on the full table,
+    which is anchored on the f64 oracle (test_ratios_against_oracle*)."""
+    from paper_1611_02665_b200.multi import (OrbitalPartition, evaluate_ratios_orbital_sharded,
+                                             shard_table_for_rank)
+
+    grid = unit_cell_grid(16)
+    rng = np.random.default_rng(9)
+    dt = DeviceTable.normal_f64(grid, 208, seed=4)
+    pos = rng.random((3000, 3)) * 2.0 - 0.5
+    coef = torch.from_numpy(rng.standard_normal((3000, 208))).cuda()
+    want = evaluate_ratios(dt, kind, pos, coef)
+    part = OrbitalPartition.make(208, 3, quantum=16)
+    total = torch.zeros_like(want)
+    for r in range(3):
+        lo, hi = part.local(r)
+        local = shard_table_for_rank(dt, part, r, tile_size=64)  # the epilogue needs 512-byte rows
+        total += evaluate_ratios_orbital_sharded(local, kind, pos, coef[:, lo:hi].contiguous())
+    assert float((total - want).abs().max() / want.abs().max()) < 1e-12  # fp64 partial sums, another order

@@ -97,3 +97,52 @@ def test_gloo_orbital_gather_and_walker_shards(world):
     assert all(p.exitcode == 0 for p in procs)
     for rank, ok_all, ok_root, ok_walk in results:
         assert ok_all and ok_root and ok_walk, (rank, ok_all, ok_root, ok_walk)
+
+
+def _ratio_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_1611_02665_b200.coeffs import FillSpec, build_table
+        from paper_1611_02665_b200.grid import GridSpec
+        from paper_1611_02665_b200.multi import sum_ratio_partials
+
+        table = build_table(GridSpec(8, 9, 10, 0.5, 0.25, 2.0), 40, FillSpec.random(13))
+        rng = np.random.default_rng(4)
+        pos = rng.random((24, 3)) * 5.0
+        coef = rng.standard_normal((24, 40))
+        full = oracle.eval_f32("vgh", table.data, table.grid.spacings, pos)[:, :, :40].astype(np.float64)
+        want = np.einsum("psn,pn->ps", full, coef)
+        bound = np.einsum("psn,pn->ps", np.abs(full), np.abs(coef))
+        part = OrbitalPartition.make(40, world, quantum=16)
+        lo, hi = part.local(rank)
+        # the rank's partial contraction over its spline slice (the GPU path: evaluate_ratios)
+        mine = torch.from_numpy(np.einsum("psn,pn->ps", full[:, :, lo:hi], coef[:, lo:hi]))
+        got_all = sum_ratio_partials(mine.clone())
+        got_root = sum_ratio_partials(mine.clone(), root=0)
+        ok_all = bool((np.abs(got_all.numpy() - want) <= 1e-14 * bound).all())
+        ok_root = (got_root is None) if rank != 0 else bool((np.abs(got_root.numpy() - want) <= 1e-14 * bound).all())
+        q.put((rank, ok_all, ok_root))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_sharded_ratio_partials_sum_to_the_full_contraction(world):
+    """The orbital-sharded fused consumer's exchange step (multi.sum_ratio_partials):
+    per-rank partial contractions over the spline slices, all-reduced / reduced to
+    rank 0, equal the contraction of the full oracle outputs."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ratio_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    results = sorted(q.get(timeout=5) for _ in range(world))
+    assert all(p.exitcode == 0 for p in procs)
+    for rank, ok_all, ok_root in results:
+        assert ok_all and ok_root, (rank, ok_all, ok_root)
