@@ -667,8 +667,15 @@ extern "C" int spo_eval_ratios(int kind, int dtype, const void *table, const int
     // The line kernel's ratio epilogue only when forced (SPO_LINE=1): without
     // the output stream the per-position kernel is not power-bound, and it is
     // faster (scripts/bench_ratios.py: 6.30e10 vs 6.18e10 orbital-evals/s).
+    // V on dense batches is the exception: there the line kernel's position
+    // groups (one plane read for 3 positions, aligned to cells) make it 2-3x
+    // faster than one position per warp (profiles/r02/rank_share.md), from the
+    // densities evaluate() sends V to the line kernel at.  SPO_LINE=0 forces
+    // the per-position kernel.
     const char *env_line = getenv("SPO_LINE");
-    if (env_line && env_line[0] == '1') {
+    const double dens = (double)n_pos / ((double)n3[0] * n3[1] * n3[2]);
+    const bool dense_v = kind == SPO_KIND_V && dens >= (dtype == SPO_F64 ? 4.0 : 2.8);
+    if (env_line ? env_line[0] == '1' : dense_v) {
         const long long extra = eval_tma_ratio_bytes(kind, dtype, nb, n_tiles, n_pos);
         rc = eval_line(kind, dtype, table, geo, g, pos, n_pos, nullptr, 0, 0, nullptr, status, workspace,
                        workspace_bytes, reinterpret_cast<cudaStream_t>(stream), 0, coef, coef_stride, ratios,

@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
         __syncwarp();
         if (lane == 0) st_release_shared(&relw[g], v);
     };
-    if constexpr (KIND == SPO_KIND_V && !RATIO && VGROUP > 1) {
+    if constexpr (KIND == SPO_KIND_V && VGROUP > 1) {
         // V: groups of VGROUP consecutive sorted positions, group k of a run
         // to warp k mod CONSUMERS.  V has little math per plane, so a plane's
         // shared-memory read is most of its cost: the group reads each plane
@@ -763,7 +763,7 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
                     const unsigned char *rec = rc + min(q0 + m, it.nb - 1) * RECB;
                     const int4 cell = *reinterpret_cast<const int4 *>(rec + 36 * sizeof(T));
                     live[m] = in && cell.x >= 0;
-                    op[m] = !in ? -1 : (a.out_index ? a.out_index[cell.w] : cell.w);
+                    op[m] = !in ? -1 : (!RATIO && a.out_index ? a.out_index[cell.w] : cell.w);
                     // the a-rows of x, y, z: weights 0..3, 12..15, 24..27 (k-power: wz[0] = t_z)
                     wxp[m] = reinterpret_cast<const T *>(rec);
                     if constexpr (!WY_SMEM) load4(rec + 12 * sizeof(T), wy[m]);
@@ -860,6 +860,17 @@ __global__ void __launch_bounds__(threads<T, KP>(), 1) line_kernel(const __grid_
 #pragma unroll
                 for (int m = 0; m < VM; ++m) {
                     if (op[m] < 0) continue;
+                    if constexpr (RATIO) {
+                        // the fused consumer: this unit's dot with the position's coefficient
+                        // row (pad lanes hold 0), reduced over the warp, as the one-position path
+                        double part[1] = {(double)NAN};
+                        if (live[m]) {
+                            const T *cf = reinterpret_cast<const T *>(a.coef) + op[m] * a.coef_stride + L0;
+                            ratio_partials<1, 32>(acc[m], cf, true, part);
+                        }
+                        if (lane == 0) a.partials[(long long)it.u * a.n_pos + op[m]] = part[0];
+                        continue;
+                    }
                     T *o = reinterpret_cast<T *>(a.out) + op[m] * a.out_pos_stride + L0;
                     if (nv == W)
                         store_lane<1>(o, a.out_stream_stride, acc[m], live[m]);
@@ -1062,8 +1073,8 @@ static int launch(const CUtensorMap &map, const LArgs &a, int sms, cudaStream_t 
     if constexpr (!KP) {
         if (win > 1) return launch1<KIND, T, RATIO, false, 1, WIN_CELLS>(map, a, sms, st);
     }
-    if constexpr (KIND == SPO_KIND_V && !RATIO) {
-        const int v = a.vgroup;  // v_group_size()
+    if constexpr (KIND == SPO_KIND_V) {
+        const int v = a.vgroup;  // v_group_size(); the ratio epilogue has groups on lines only (win = 1)
         if (v == 2) return launch1<KIND, T, RATIO, KP, 2>(map, a, sms, st);
         if (v == 4) return launch1<KIND, T, RATIO, KP, 4>(map, a, sms, st);
         if (v == 3) return launch1<KIND, T, RATIO, KP, 3>(map, a, sms, st);
@@ -1203,7 +1214,7 @@ int eval_line(int kind, int dtype, const void *table, const TableGeom &geo, cons
     const bool kpower = geo.kmul != 1;
     const double dens = (double)n_pos / ((double)geo.nx * geo.ny * geo.nz);
     int vgroup = 1, cellgroups = 0;
-    if (kind == SPO_KIND_V && !ratio) {
+    if (kind == SPO_KIND_V && (!ratio || win == 1)) {
         const char *env_cell = getenv("SPO_VCELL");
         // (fp32 k-power tables keep fixed groups of 4: aligned groups of 3 measured +2..4% there,
         // fp64 k-power -9%)

@@ -98,6 +98,44 @@ def test_ratios_line_path(torch, monkeypatch, kind, dtype):
     assert float((a[ok.cuda()] - want).abs().max() / want.abs().max()) < rtol
 
 
+@pytest.mark.parametrize("per_cell", [3, 10])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_ratios_v_position_groups(torch, monkeypatch, dtype, per_cell):
+    """V on dense batches: the ratio epilogue inside the line kernel's V position
+    groups (fixed groups at 3 per cell, groups aligned to cells at 10 per cell,
+    both forced too): bitwise equal to the per-position kernel's ratios, NaN
+    rows for non-finite positions, and equal to the contracted outputs."""
+    grid = unit_cell_grid(12)
+    rng = np.random.default_rng(21)
+    if dtype == "f32":
+        dt = DeviceTable.random(grid, 300, seed=3, tile_size=128)
+        tdt, rtol = torch.float32, 1e-6
+    else:
+        dt = DeviceTable.normal_f64(grid, 144, seed=3, tile_size=64)
+        tdt, rtol = torch.float64, 1e-12
+    P = per_cell * 12 ** 3 + 37
+    pos = rng.random((P, 3)) * 2.0 - 0.5
+    pos[[5, P - 1]] = np.nan
+    dpos = torch.from_numpy(pos).cuda()
+    coef = torch.from_numpy(rng.standard_normal((P, dt.n_splines))).to("cuda", tdt)
+    monkeypatch.setenv("SPO_LINE", "0")
+    ref = evaluate_ratios(dt, "v", dpos, coef, check=False)
+    monkeypatch.setenv("SPO_LINE", "1")
+    for knobs in ({}, {"SPO_VCELL": "0"}, {"SPO_VCELL": "1"}, {"SPO_VGROUP": "1"}, {"SPO_VGROUP": "4", "SPO_VCELL": "1"}):
+        for k, v in knobs.items():
+            monkeypatch.setenv(k, v)
+        got = evaluate_ratios(dt, "v", dpos, coef, check=False)
+        for k in knobs:
+            monkeypatch.delenv(k)
+        assert torch.equal(got.nan_to_num(7.0), ref.nan_to_num(7.0)), knobs
+        assert bool(torch.isnan(got[5]).all()) and bool(torch.isnan(got[P - 1]).all())
+    monkeypatch.delenv("SPO_LINE")
+    ok = np.ones(P, bool)
+    ok[[5, P - 1]] = False
+    want = reference_ratios(torch, dt, "v", pos[ok], coef[torch.from_numpy(ok).cuda()])
+    assert float((ref[torch.from_numpy(ok).cuda()] - want).abs().max() / want.abs().max()) < rtol
+
+
 @pytest.mark.parametrize("line", ["0", "1"])
 @pytest.mark.parametrize("kind", ["v", "vgl", "vgh"])
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
